@@ -1,0 +1,93 @@
+"""Hand-built scenes and the parity comparator (test helpers; no method arithmetic)."""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2605_13600_b200 import synth
+
+NONE = 0xFFFFFFFF
+
+
+def gaussians(means, scales, rots, opac) -> synth.Gaussians:
+    return synth.Gaussians(np.asarray(means, np.float32).reshape(-1, 3),
+                           np.asarray(scales, np.float32).reshape(-1, 3),
+                           np.asarray(rots, np.float32).reshape(-1, 4),
+                           np.asarray(opac, np.float32).reshape(-1))
+
+
+def identity_camera(W, H, f=100.0, cx=None, cy=None) -> synth.Camera:
+    return synth.Camera(f, f, W / 2.0 if cx is None else cx, H / 2.0 if cy is None else cy, W, H,
+                        np.eye(4, dtype=np.float32))
+
+
+def full_frame_codes(code_per_view, S=None):
+    """One region (id 0) per view with the given [(atom, coef), ...] code."""
+    S = S or max(len(c) for c in code_per_view)
+    V = len(code_per_view)
+    atoms = np.full((V, S), NONE, np.uint32)
+    coefs = np.zeros((V, S), np.float32)
+    for v, code in enumerate(code_per_view):
+        for s, (a, c) in enumerate(code):
+            atoms[v, s] = a
+            coefs[v, s] = c
+    return synth.Codes(atoms, coefs, np.arange(V, dtype=np.int64), np.ones(V, np.int32))
+
+
+def compare_accumulators(W_gpu, Z_gpu, W_ora, Z_ora, rtol=1e-4, atol=1e-6):
+    """|x_gpu - x_ora| <= atol + rtol |x_ora| for every element (north_star tolerance)."""
+    W_gpu = np.asarray(W_gpu, np.float64)
+    Z_gpu = np.asarray(Z_gpu, np.float64)
+    dW = np.abs(W_gpu - W_ora) - (atol + rtol * np.abs(W_ora))
+    dZ = np.abs(Z_gpu - Z_ora) - (atol + rtol * np.abs(Z_ora))
+    bad_w = np.argwhere(dW > 0)
+    bad_z = np.argwhere(dZ > 0)
+    return bad_w, bad_z
+
+
+def compare_codes(atoms_gpu, coefs_gpu, W_ora, K, rtol=1e-4, atol=1e-6):
+    """SURVEY.md §8(c) comparator, step 3.  Returns (n_mismatch, n_tie_allowance, worst_msg).
+
+    The GPU's atom set must equal the oracle's positive-Top-K set, except that atoms whose
+    oracle value is within tol = atol + rtol*v_K of v_K may be exchanged; coefficients of
+    matched atoms must agree within atol + rtol*w (w recomputed from the oracle's fp64 W
+    restricted to the GPU's chosen set, so an allowed exchange is not double-counted)."""
+    G, L = W_ora.shape
+    atoms_gpu = np.asarray(atoms_gpu).astype(np.int64) & 0xFFFFFFFF
+    coefs_gpu = np.asarray(coefs_gpu, np.float64)
+    bad, ties, worst = 0, 0, ""
+    for i in range(G):
+        w = W_ora[i]
+        order = sorted([a for a in range(L) if w[a] > 0], key=lambda a: (-w[a], a))
+        top = order[:K]
+        sel = [int(a) for a in atoms_gpu[i] if a != NONE]
+        if not top:
+            if sel or np.any(coefs_gpu[i] != 0):
+                bad += 1
+                worst = worst or f"row {i}: expected empty code, got {sel}"
+            continue
+        vK = w[top[-1]]
+        tol = atol + rtol * vK
+        ok = len(sel) == len(top) and len(set(sel)) == len(sel)
+        if ok and set(sel) != set(top):
+            # exchanges only among near-ties of the K-th value
+            for a in set(sel) ^ set(top):
+                if abs(w[a] - vK) > tol:
+                    ok = False
+            if ok:
+                ties += 1
+        if ok:
+            denom = sum(w[a] for a in sel)
+            for s, a in enumerate(sel):
+                ref = w[a] / denom
+                if abs(coefs_gpu[i, s] - ref) > atol + rtol * ref:
+                    ok = False
+            # descending order of the stored coefficients
+            if any(coefs_gpu[i, s] < coefs_gpu[i, s + 1] for s in range(len(sel) - 1)):
+                ok = False
+            if any(a != NONE for a in atoms_gpu[i, len(sel):]) or np.any(coefs_gpu[i, len(sel):] != 0):
+                ok = False
+        if not ok:
+            bad += 1
+            if not worst:
+                worst = f"row {i}: gpu {list(zip(sel, coefs_gpu[i][:len(sel)]))} vs oracle top {[(a, w[a]) for a in top]}"
+    return bad, ties, worst
