@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: SCOUP scene uplift (weighted sparse aggregation) on B200.
+
+One step = one full scene uplift of BASELINE.json configs[3] ("outdoor": 3M Gaussians,
+300 views at 1600x1066, L=64, S=K=8): every view rasterised and aggregated (Eq. 5 /
+Algorithm 1), then Eq. 6 Top-K on every Gaussian.  With N ranks the views are sharded
+(v = rank mod N), the fp32 partial sums are combined by an NCCL reduce-scatter and each
+rank finalises its Gaussian shard.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config outdoor] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scene uplift seconds & pixel-Gaussian contributions/s at 1/2/4/8 B200"
+# algorithmic lane-ops of the spec per support test and per contribution
+OPS_PER_TEST = 28
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="outdoor")
+    ap.add_argument("--views", type=int, default=0, help="limit the number of views (quick runs only)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-views", type=int, default=1, help="views in the oracle cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def crop_band(cam, y0, y1):
+    """The rows [y0, y1) of a view as a camera of its own (same rays; principal point shifted)."""
+    from paper_2605_13600_b200 import synth
+    return synth.Camera(cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.width, y1 - y0, cam.world_to_camera)
+
+
+def cpu_baseline(cfg, scene, views, seed=0, band=3):
+    """The oracle as it stands, single-threaded, on a bounded sample: the middle third of the
+    rows of each listed view (full Gaussian set, full width; ~15 s per outdoor view band)."""
+    import oracle
+    from paper_2605_13600_b200 import synth
+    import torch
+    maps = synth.make_region_maps_torch(cfg, torch.device("cpu"), seed=seed, views=views).numpy().view(np.uint32)
+    y0 = cfg.height // 2 - cfg.height // (2 * band)
+    y1 = y0 + cfg.height // band
+    maps = np.ascontiguousarray(maps[:, y0:y1])
+    codes = synth.make_codes(cfg, seed=seed, views=views)
+    cams = [crop_band(scene.cameras[v], y0, y1) for v in views]
+    t0 = time.perf_counter()
+    W, Z, frags = oracle.uplift_accumulate(scene.gaussians, cams, maps, codes.atoms,
+                                           codes.coefs, codes.row0, codes.num_regions, cfg.L, cfg.K)
+    dt = time.perf_counter() - t0
+    return {"value": float(frags.sum()) / dt, "unit": "contributions/s", "cores": 1, "kind": "oracle",
+            "sample": f"rows {y0}..{y1} of views {views} of {cfg.name} ({cfg.num_gaussians} Gaussians, "
+                      f"{cfg.width}x{cfg.height}), accumulation, {dt:.1f} s single-threaded",
+            "seconds": dt, "contributions": int(frags.sum())}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_2605_13600_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.views:
+        cfg = cfg.with_(num_views=args.views)
+    scene = synth.make_scene(cfg, 0)
+    vals = []
+    per = []
+    for s in range(args.warmup + args.steps):
+        v = [s % cfg.num_views]
+        r = cpu_baseline(cfg, scene, v)
+        if s >= args.warmup:
+            vals.append(r["value"])
+            per.append(r)
+    value = statistics.median(vals)
+    ms = statistics.median([r["seconds"] for r in per]) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "contributions/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "gaussians": cfg.num_gaussians, "views": cfg.num_views,
+                       "width": cfg.width, "height": cfg.height, "L": cfg.L, "K": cfg.K,
+                       "step": "one view of the workload per step (bounded sample)"},
+            "cpu_baseline": {"value": value, "unit": "contributions/s", "cores": 1, "kind": "oracle",
+                             "sample": "per step the middle third of one view's rows (all Gaussians), views 0.."
+                                       + str(args.warmup + args.steps - 1)},
+            "e2e": {"value": value, "unit": "contributions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2605_13600_b200 import synth
+    from paper_2605_13600_b200.uplift import SparseUplift
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    if args.views:
+        cfg = cfg.with_(num_views=args.views)
+    scene = synth.make_scene(cfg, 0)
+    g = scene.gaussians
+    G, L, K = g.count, cfg.L, cfg.K
+    my_views = list(range(rank, cfg.num_views, world))
+    cams = [scene.cameras[v] for v in my_views]
+    maps = synth.make_region_maps_torch(cfg, dev, seed=0, views=my_views)
+    codes_h = synth.make_codes(cfg, seed=0, views=my_views)
+    codes = synth.Codes(torch.from_numpy(codes_h.atoms.view(np.int32)).to(dev), torch.from_numpy(codes_h.coefs).to(dev),
+                        codes_h.row0, codes_h.num_regions)
+    gd = synth.Gaussians(*[torch.from_numpy(a).to(dev) for a in (g.means, g.scales, g.rotations, g.opacities)])
+    Npad = int(math.ceil(G / world) * world)
+    shard = Npad // world
+    up = SparseUplift(gd, L, K, device=local, rows_padded=Npad)
+    Ws = torch.empty((shard, L), dtype=torch.float32, device=dev) if world > 1 else None
+    Zs = torch.empty((shard,), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def step():
+        up.reset()
+        up.add_views(cams, maps, codes)
+        if world > 1:
+            dist.reduce_scatter_tensor(Ws, up.W)
+            dist.reduce_scatter_tensor(Zs, up.Z)
+            return up.finalize(first_row=rank * shard, num_rows=shard, W_rows=Ws, Z_rows=Zs)
+        return up.finalize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = up.stats()  # one step's counters (reset at each step start)
+    contrib_step = sum_over_ranks(st["contributions"])
+    tests_step = sum_over_ranks(st["support_tests"])
+
+    up.set_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    elapsed_ms = max_over_ranks(e0.elapsed_time(e1))
+    tm = up.timing()
+    st = up.stats()
+    ms_per_step = elapsed_ms / args.steps
+    value = contrib_step * args.steps / (elapsed_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (fused raster-aggregate), live CUDA-event timing
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * 128 * sm_max * 1e6 / 1e12  # T lane-ops/s
+    launches = max(1, tm["raster_launches"])
+    ras_avg_s = tm["raster_ms"] / launches / 1e3
+    ops_per_launch = (OPS_PER_TEST * st["support_tests"] + (2 * cfg.S + 1) * st["contributions"]) / max(1, st["views"])
+    achieved = ops_per_launch / ras_avg_s / 1e12 if ras_avg_s > 0 else 0.0
+    total_dev_ms = tm["preprocess_ms"] + tm["binning_ms"] + tm["raster_ms"] + tm["topk_ms"]
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        maps_h = maps.cpu().pin_memory()
+        g_h = synth.Gaussians(*[torch.from_numpy(a).pin_memory() for a in (g.means, g.scales, g.rotations, g.opacities)])
+        atoms_h = torch.empty((Npad if world == 1 else shard, K), dtype=torch.int32).pin_memory()
+        coefs_h = torch.empty((Npad if world == 1 else shard, K), dtype=torch.float32).pin_memory()
+        ca_h = torch.from_numpy(codes_h.atoms.view(np.int32)).pin_memory()
+        cc_h = torch.from_numpy(codes_h.coefs).pin_memory()
+        codes_hp = synth.Codes(ca_h, cc_h, codes_h.row0, codes_h.num_regions)
+        nrows = G if world == 1 else shard
+
+        def e2e_step():
+            u2 = SparseUplift(g_h, L, K, device=local, rows_padded=Npad)
+            u2.add_views(cams, maps_h, codes_hp)
+            if world > 1:
+                dist.reduce_scatter_tensor(Ws, u2.W)
+                dist.reduce_scatter_tensor(Zs, u2.Z)
+                u2.finalize(first_row=rank * shard, num_rows=shard, W_rows=Ws, Z_rows=Zs,
+                            out_atoms=atoms_h[:shard], out_coefs=coefs_h[:shard])
+            else:
+                u2.finalize(0, G, out_atoms=atoms_h[:G], out_coefs=coefs_h[:G])
+            u2.close()
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 2))):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        n_e2e = max(1, min(args.steps, 2))
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / n_e2e)
+        h2d = sum_over_ranks(maps_h.numel() * 4 + G * 44 + ca_h.numel() * 8)
+        d2h = sum_over_ranks(nrows * K * 8)
+        e2e = {"value": contrib_step / e2e_s, "unit": "contributions/s", "seconds_per_step": e2e_s,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, scene, list(range(args.cpu_views)))
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "contributions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "scene_uplift_s": ms_per_step / 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "gaussians": G, "views": cfg.num_views, "width": cfg.width,
+                       "height": cfg.height, "L": L, "S": cfg.S, "K": K, "regions_per_view": cfg.regions[0],
+                       "parallelism": f"view-sharded x{world} + reduce-scatter" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (region maps %.2f GB, W %.0f MB per GPU)" % (
+                           maps.numel() * 4 / 1e9, Npad * L * 4 / 1e6)},
+            "contributions_per_step": int(contrib_step),
+            "support_tests_per_step": int(tests_step),
+            "device_ms_per_step": {k: tm[k] / args.steps for k in ("preprocess_ms", "binning_ms", "raster_ms", "topk_ms")},
+            "roofline": {"bound": "alu", "kernel": "raster_aggregate_kernel", "achieved": achieved,
+                         "peak": alu_peak, "unit": "T lane-ops/s", "frac": achieved / alu_peak,
+                         "traffic": None, "avg_launch_ms": ras_avg_s * 1e3,
+                         "share_of_step": tm["raster_ms"] / max(1e-9, total_dev_ms),
+                         "peak_source": f"{sms} SMs x 128 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
+            "gpu_launches": int((st["kernel_launches"] + st["cub_launches"]) / max(1, args.steps)),
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    up.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

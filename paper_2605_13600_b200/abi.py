@@ -1,0 +1,174 @@
+"""Thin ctypes binding of libscoup.so (include/scoup.h) -- argument marshalling only.
+
+Every step of the path runs in the CUDA library; this module converts torch tensors /
+numpy arrays to pointers and status codes to exceptions.  There is no fallback: if the
+extension is missing or fails to load, `lib()` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libscoup.so")
+
+SCOUP_NONE = 0xFFFFFFFF
+STATUS = {0: "SCOUP_OK", 1: "SCOUP_EINVAL", 2: "SCOUP_EDATA", 3: "SCOUP_ECUDA", 4: "SCOUP_ENOMEM",
+          5: "SCOUP_ESTATE", 6: "SCOUP_EUNSUPPORTED"}
+
+
+class ScoupError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class scoup_camera(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32), ("world_to_camera", C.c_float * 16)]
+
+
+class scoup_stats(C.Structure):
+    _fields_ = [("views", C.c_int64), ("contributions", C.c_int64), ("tile_entries", C.c_int64),
+                ("visible", C.c_int64), ("support_tests", C.c_int64), ("kernel_launches", C.c_int64),
+                ("cub_launches", C.c_int64)]
+
+
+class scoup_timing(C.Structure):
+    _fields_ = [("preprocess_ms", C.c_double), ("binning_ms", C.c_double), ("raster_ms", C.c_double),
+                ("topk_ms", C.c_double), ("raster_launches", C.c_int64), ("views_timed", C.c_int64)]
+
+
+EXPORTS = ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
+           "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
+           "scoup_uplift_set_timing", "scoup_uplift_get_timing",
+           "scoup_uplift_free", "scoup_last_error", "scoup_version"]
+
+_lib = None
+
+
+def lib():
+    """Load libscoup.so (raises if it is missing -- there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libscoup.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.scoup_uplift_init.argtypes = [C.c_int, P, i64, P, P, P, P, i32, i32, P, P, i64, C.POINTER(P)]
+        L.scoup_uplift_add_views.argtypes = [P, i32, P, P, P, P, P, P, i32, P]
+        L.scoup_uplift_finalize_topk.argtypes = [P, i64, i64, P, P, P, P]
+        L.scoup_uplift_reset.argtypes = [P]
+        L.scoup_uplift_get_accumulators.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(i64)]
+        L.scoup_uplift_get_stats.argtypes = [P, C.POINTER(scoup_stats)]
+        L.scoup_uplift_set_timing.argtypes = [P, C.c_int]
+        L.scoup_uplift_get_timing.argtypes = [P, C.POINTER(scoup_timing)]
+        L.scoup_uplift_free.argtypes = [P]
+        L.scoup_uplift_free.restype = None
+        L.scoup_last_error.restype = C.c_char_p
+        L.scoup_version.restype = C.c_char_p
+        for name in ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
+                     "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
+                     "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise ScoupError(status, lib().scoup_last_error().decode())
+
+
+def ptr(x) -> Optional[int]:
+    """Raw pointer of a torch tensor / numpy array (must be contiguous), or None."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    raise TypeError(type(x))
+
+
+def cameras_struct(cams: Sequence) -> C.Array:
+    arr = (scoup_camera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i].fx, arr[i].fy, arr[i].cx, arr[i].cy = c.fx, c.fy, c.cx, c.cy
+        arr[i].width, arr[i].height = c.width, c.height
+        w = np.asarray(c.world_to_camera, dtype=np.float32).ravel()
+        for k in range(16):
+            arr[i].world_to_camera[k] = float(w[k])
+    return arr
+
+
+# ---- the C entry points, same names -------------------------------------------------
+
+def scoup_uplift_init(device: int, stream: int, num_gaussians: int, means, scales, rotations, opacities,
+                      L: int, K: int, W=None, Z=None, rows_padded: int = 0) -> int:
+    h = C.c_void_p()
+    _check(lib().scoup_uplift_init(device, stream or None, num_gaussians, ptr(means), ptr(scales),
+                                   ptr(rotations), ptr(opacities), L, K, ptr(W), ptr(Z), rows_padded,
+                                   C.byref(h)))
+    return h.value
+
+
+def scoup_uplift_add_views(h: int, cameras: Sequence, region_ids, code_row0, num_regions, code_atoms,
+                           code_coefs, S: int, contributions_out=None) -> None:
+    row0 = np.ascontiguousarray(code_row0, dtype=np.int64)
+    nreg = np.ascontiguousarray(num_regions, dtype=np.int32)
+    cams = cameras_struct(cameras)
+    _check(lib().scoup_uplift_add_views(h, len(cameras), cams, ptr(region_ids), ptr(row0), ptr(nreg),
+                                        ptr(code_atoms), ptr(code_coefs), S, ptr(contributions_out)))
+
+
+def scoup_uplift_finalize_topk(h: int, first_row: int, num_rows: int, W_rows, Z_rows, out_atoms,
+                               out_coefs) -> None:
+    _check(lib().scoup_uplift_finalize_topk(h, first_row, num_rows, ptr(W_rows), ptr(Z_rows),
+                                            ptr(out_atoms), ptr(out_coefs)))
+
+
+def scoup_uplift_reset(h: int) -> None:
+    _check(lib().scoup_uplift_reset(h))
+
+
+def scoup_uplift_get_accumulators(h: int):
+    W, Z, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+    _check(lib().scoup_uplift_get_accumulators(h, C.byref(W), C.byref(Z), C.byref(n)))
+    return W.value, Z.value, n.value
+
+
+def scoup_uplift_get_stats(h: int) -> dict:
+    s = scoup_stats()
+    _check(lib().scoup_uplift_get_stats(h, C.byref(s)))
+    return {k: getattr(s, k) for k, _ in scoup_stats._fields_}
+
+
+def scoup_uplift_set_timing(h: int, enable: bool) -> None:
+    _check(lib().scoup_uplift_set_timing(h, 1 if enable else 0))
+
+
+def scoup_uplift_get_timing(h: int) -> dict:
+    t = scoup_timing()
+    _check(lib().scoup_uplift_get_timing(h, C.byref(t)))
+    return {k: getattr(t, k) for k, _ in scoup_timing._fields_}
+
+
+def scoup_uplift_free(h: int) -> None:
+    if h:
+        lib().scoup_uplift_free(h)
+
+
+def scoup_last_error() -> str:
+    return lib().scoup_last_error().decode()
+
+
+def scoup_version() -> str:
+    return lib().scoup_version().decode()

@@ -1,0 +1,719 @@
+// api.cu -- C ABI (include/scoup.h) and host orchestration of the sm_100a path.
+//
+// Per view (Algorithm 1 lines 5-12):
+//   stage 1  preprocess (EWA, culls, support rect)  ->  depth sort (CUB radix, stable, so
+//            equal depths keep index order)  ->  scan of tile counts in depth
+//            order  ->  entry total copied to pinned host memory
+//   stage 2  emit (Gaussian, tile) entries in depth order  ->  stable radix sort on the tile
+//            id  ->  per-tile ranges  ->  fused rasterise-and-aggregate kernel
+// Stage 2 needs the entry total on the host (CUB takes host-side sizes), so two view
+// contexts on two streams are software-pipelined: while the host waits for view v's total,
+// the GPU runs view v-1's raster.
+// finalize_topk runs Eq. 6 on the requested rows.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/scoup.h"
+#include "internal.cuh"
+
+using namespace scoup;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+scoup_status fail(scoup_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+struct CudaError {
+    cudaError_t err;
+    std::string where;
+};
+
+#define CK(expr)                                                    \
+    do {                                                            \
+        cudaError_t _e = (expr);                                    \
+        if (_e != cudaSuccess) throw CudaError{_e, #expr};          \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+void grow(T** ptr, size_t* cap, size_t need, double slack = 1.25) {
+    if (need <= *cap && *ptr) return;
+    size_t n = std::max<size_t>(need, (size_t)((double)need * slack));
+    if (*ptr) CK(cudaFree(*ptr));
+    *ptr = nullptr;
+    *cap = 0;
+    CK(cudaMalloc((void**)ptr, std::max<size_t>(n, 1) * sizeof(T)));
+    *cap = n;
+}
+
+struct Ctx {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev_total = nullptr;
+    ViewBuffers vb{};
+    size_t g_cap = 0, e_cap = 0, t_cap = 0;
+    void* cub_tmp = nullptr;
+    size_t cub_cap = 0;
+    uint64_t* h_total = nullptr;  // pinned
+    uint32_t* ids_stage = nullptr;
+    size_t ids_cap = 0;
+    // per-view launch state for stage 2
+    int view = -1;
+    const uint32_t* ids_dev = nullptr;
+    // timing: ring of event sets (start/end of stage 1, binning start, raster start/end)
+    struct EvSet { cudaEvent_t e[5]; bool pending; };
+    std::vector<EvSet> evs;
+    int ev_next = 0;
+    int ev_cur = -1;
+};
+
+}  // namespace
+
+struct scoup_uplift {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t G = 0, Npad = 0;
+    int L = 0, K = 0;
+    float* W = nullptr;
+    float* Z = nullptr;
+    bool own_wz = false;
+    PackedGaussians pg{};
+    int* d_err_code = nullptr;
+    long long* d_err_index = nullptr;
+    unsigned long long* d_stats = nullptr;  // views, contributions, entries, visible
+    Ctx ctx[2];
+    uint32_t* code_atoms = nullptr;
+    float* code_coefs = nullptr;
+    size_t code_cap = 0;
+    uint32_t* code_atoms_in = nullptr;
+    float* code_coefs_in = nullptr;
+    int64_t host_entries = 0;
+    cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+    bool latched = false;
+    int sms = 148;
+    // timing + launch accounting
+    bool timing = false;
+    double t_pre = 0, t_bin = 0, t_ras = 0, t_topk = 0;
+    int64_t ras_launches = 0, views_timed = 0;
+    cudaEvent_t topk_ev[2] = {nullptr, nullptr};
+    bool topk_pending = false;
+    int64_t kernel_launches = 0, cub_launches = 0;
+};
+
+namespace {
+
+ErrorLatch latch_of(scoup_uplift* h) { return ErrorLatch{h->d_err_code, h->d_err_index}; }
+
+scoup_status check_latched(scoup_uplift* h) {
+    int code = 0;
+    long long idx = 0;
+    CK(cudaMemcpy(&code, h->d_err_code, sizeof(int), cudaMemcpyDeviceToHost));
+    if (code == ERR_NONE) return SCOUP_OK;
+    CK(cudaMemcpy(&idx, h->d_err_index, sizeof(long long), cudaMemcpyDeviceToHost));
+    h->latched = true;
+    const char* what = code == ERR_GAUSSIAN ? "non-finite or invalid Gaussian parameters at Gaussian index "
+                       : code == ERR_REGION ? "region id >= num_regions at flat pixel index "
+                                            : "invalid code slot (atom >= L or bad coefficient) at flat slot index ";
+    return fail(SCOUP_EDATA, std::string("data error: ") + what + std::to_string(idx));
+}
+
+void ctx_init(Ctx& c) {
+    CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c.ev_total, cudaEventDisableTiming));
+    CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t)));
+}
+
+void ctx_free(Ctx& c) {
+    for (auto& es : c.evs)
+        for (int k = 0; k < 5; k++) cudaEventDestroy(es.e[k]);
+    c.evs.clear();
+    ViewBuffers& b = c.vb;
+    void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect,
+                    b.rec0, b.rec1, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp, c.ids_stage};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c.h_total) cudaFreeHost(c.h_total);
+    if (c.ev_total) cudaEventDestroy(c.ev_total);
+    if (c.s) cudaStreamDestroy(c.s);
+    c = Ctx{};
+}
+
+void ctx_reserve_gaussians(Ctx& c, int64_t G) {
+    if ((size_t)G <= c.g_cap && c.vb.depth_key) return;
+    size_t cap = 0;
+    ViewBuffers& b = c.vb;
+    size_t n = std::max<int64_t>(G, 1);
+#define RG(f) { size_t cc = 0; b.f = nullptr; grow(&b.f, &cc, n, 1.0); }
+    if (b.depth_key) {
+        void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect, b.rec0, b.rec1};
+        for (void* p : ptrs) CK(cudaFree(p));
+    }
+    RG(depth_key) RG(depth_key_alt) RG(gidx) RG(gidx_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1)
+#undef RG
+    (void)cap;
+    c.g_cap = n;
+}
+
+void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes); }
+
+bool rigid_ok(const float* M) {
+    double R[3][3];
+    for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) R[a][b] = M[4 * a + b];
+    for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) {
+            double d = 0;
+            for (int k = 0; k < 3; k++) d += R[a][k] * R[b][k];
+            if (std::fabs(d - (a == b ? 1.0 : 0.0)) > 1e-5) return false;
+        }
+    double det = R[0][0] * (R[1][1] * R[2][2] - R[1][2] * R[2][1]) - R[0][1] * (R[1][0] * R[2][2] - R[1][2] * R[2][0]) +
+                 R[0][2] * (R[1][0] * R[2][1] - R[1][1] * R[2][0]);
+    if (std::fabs(det - 1.0) > 1e-5) return false;
+    for (int k = 0; k < 16; k++)
+        if (!std::isfinite(M[k])) return false;
+    return true;
+}
+
+Camera to_cam(const scoup_camera& c) {
+    Camera k;
+    k.fx = c.fx; k.fy = c.fy; k.cx = c.cx; k.cy = c.cy;
+    k.width = c.width; k.height = c.height;
+    for (int i = 0; i < 12; i++) k.P[i] = c.world_to_camera[i];
+    return k;
+}
+
+int bits_for(uint32_t n) {
+    int b = 1;
+    while ((1u << b) < n && b < 32) b++;
+    return b;
+}
+
+constexpr int EV_RING = 8;
+
+void ev_accumulate(scoup_uplift* h, Ctx::EvSet& es) {
+    if (!es.pending) return;
+    CK(cudaEventSynchronize(es.e[4]));
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, es.e[0], es.e[1]));
+    CK(cudaEventElapsedTime(&b, es.e[2], es.e[3]));
+    CK(cudaEventElapsedTime(&c, es.e[3], es.e[4]));
+    h->t_pre += a;
+    h->t_bin += b;
+    h->t_ras += c;
+    h->ras_launches++;
+    h->views_timed++;
+    es.pending = false;
+}
+
+Ctx::EvSet* ev_begin(scoup_uplift* h, Ctx& c) {
+    if (!h->timing) { c.ev_cur = -1; return nullptr; }
+    if (c.evs.empty()) {
+        c.evs.resize(EV_RING);
+        for (auto& es : c.evs) {
+            for (int k = 0; k < 5; k++) CK(cudaEventCreate(&es.e[k]));
+            es.pending = false;
+        }
+    }
+    c.ev_cur = c.ev_next;
+    c.ev_next = (c.ev_next + 1) % EV_RING;
+    Ctx::EvSet& es = c.evs[c.ev_cur];
+    ev_accumulate(h, es);
+    return &es;
+}
+
+Ctx::EvSet* ev_cur(Ctx& c) { return c.ev_cur >= 0 ? &c.evs[c.ev_cur] : nullptr; }
+
+// Stage 1 of one view: preprocess, depth sort, scan -> total entries (async to pinned host).
+void stage1(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int tiles_y) {
+    const int64_t G = h->G;
+    ViewBuffers& b = c.vb;
+    Ctx::EvSet* es = ev_begin(h, c);
+    if (es) CK(cudaEventRecord(es->e[0], c.s));
+    launch_preprocess(h->pg, G, cam, tiles_x, tiles_y, b, h->d_stats + 3, c.s);
+    size_t need = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, (int)G, 0, 32, c.s));
+    size_t need2 = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)G, c.s));
+    ctx_reserve_cub(c, std::max(need, need2));
+    CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, (int)G, 0, 32, c.s));
+    launch_gather_scan_input(b.gidx_sorted, b.tiles, b.offsets, G, c.s);
+    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)G, c.s));
+    CK(cudaMemcpyAsync(c.h_total, b.offsets + (G - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    if (es) CK(cudaEventRecord(es->e[1], c.s));
+    CK(cudaEventRecord(c.ev_total, c.s));
+    h->kernel_launches += 2;
+    h->cub_launches += 2;
+}
+
+// Stage 2: emit, tile sort, ranges, raster.  Requires stage 1's total on the host.
+scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int tiles_y, const uint32_t* ids,
+                    int64_t code_row0, int32_t num_regions, int S, long long* contrib_out, long long pixel_base) {
+    CK(cudaEventSynchronize(c.ev_total));
+    const uint64_t E = *c.h_total;
+    const int ntiles = tiles_x * tiles_y;
+    ViewBuffers& b = c.vb;
+    if (E >= (uint64_t)INT32_MAX)
+        return fail(SCOUP_EUNSUPPORTED, "view produces " + std::to_string(E) + " tile entries (>= 2^31)");
+    grow(&b.ranges, &c.t_cap, (size_t)ntiles, 1.0);
+    h->host_entries += (int64_t)E;
+    Ctx::EvSet* es = ev_cur(c);
+    if (es) CK(cudaEventRecord(es->e[2], c.s));
+    if (E > 0) {
+        if (E > c.e_cap || !b.ekey) {
+            size_t cap = c.e_cap;
+            size_t n = (size_t)((double)E * 1.25);
+            void* ptrs[] = {b.ekey, b.eval, b.ekey_alt, b.eval_alt};
+            for (void* p : ptrs)
+                if (p) CK(cudaFree(p));
+            b.ekey = b.eval = b.ekey_alt = b.eval_alt = nullptr;
+            CK(cudaMalloc((void**)&b.ekey, n * 4));
+            CK(cudaMalloc((void**)&b.eval, n * 4));
+            CK(cudaMalloc((void**)&b.ekey_alt, n * 4));
+            CK(cudaMalloc((void**)&b.eval_alt, n * 4));
+            (void)cap;
+            c.e_cap = n;
+        }
+        launch_emit(b.gidx_sorted, b.offsets, b.rect, tiles_x, h->G, b.ekey, b.eval, c.s);
+        const int nbits = bits_for((uint32_t)ntiles);
+        size_t need = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
+        ctx_reserve_cub(c, need);
+        CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
+        CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * ntiles, c.s));
+        launch_ranges(b.ekey_alt, (int64_t)E, b.ranges, c.s);
+        RasterParams p{};
+        p.cam = cam;
+        p.tiles_x = tiles_x;
+        p.tiles_y = tiles_y;
+        p.ranges = b.ranges;
+        p.eval = b.eval_alt;
+        p.rec0 = b.rec0;
+        p.rec1 = b.rec1;
+        p.region_ids = ids;
+        p.code_atoms = h->code_atoms;
+        p.code_coefs = h->code_coefs;
+        p.code_row0 = code_row0;
+        p.num_regions = num_regions;
+        p.S = S;
+        p.L = h->L;
+        p.W = h->W;
+        p.Z = h->Z;
+        p.contrib_ctr = h->d_stats + 1;
+        p.contrib_out = contrib_out;
+        p.err = latch_of(h);
+        p.pixel_base = pixel_base;
+        p.support_ctr = h->d_stats + 4;
+        if (es) CK(cudaEventRecord(es->e[3], c.s));
+        launch_raster(p, c.s);
+        h->kernel_launches += 3;
+        h->cub_launches += 1;
+    } else if (es) {
+        CK(cudaEventRecord(es->e[3], c.s));
+    }
+    if (es) {
+        CK(cudaEventRecord(es->e[4], c.s));
+        es->pending = true;
+    }
+    CK(cudaGetLastError());
+    return SCOUP_OK;
+}
+
+__global__ void add_u64(unsigned long long* p, unsigned long long v) { atomicAdd(p, v); }
+
+}  // namespace
+
+extern "C" {
+
+const char* scoup_last_error(void) { return g_last_error.c_str(); }
+
+const char* scoup_version(void) { return "scoup-b200 0.1.0 (sm_100a)"; }
+
+scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussians, const float* means,
+                               const float* scales, const float* rotations, const float* opacities, int32_t L,
+                               int32_t K, float* W, float* Z, int64_t rows_padded, scoup_uplift** out) {
+    g_last_error.clear();
+    if (!out) return fail(SCOUP_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_gaussians < 0) return fail(SCOUP_EINVAL, "num_gaussians < 0");
+    if (num_gaussians > 0 && (!means || !scales || !rotations || !opacities))
+        return fail(SCOUP_EINVAL, "Gaussian parameter pointer is NULL");
+    if (K < 1) return fail(SCOUP_EINVAL, "K < 1");
+    if (L < 1) return fail(SCOUP_EINVAL, "L < 1");
+    if (K > L) return fail(SCOUP_EINVAL, "K > L (SPEC.md:291)");
+    if (L > SCOUP_MAX_L || K > SCOUP_MAX_K) return fail(SCOUP_EUNSUPPORTED, "L or K beyond implementation limits");
+    if (num_gaussians >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "num_gaussians >= 2^31");
+    if (rows_padded == 0) rows_padded = num_gaussians;
+    if (rows_padded < num_gaussians) return fail(SCOUP_EINVAL, "rows_padded < num_gaussians");
+    if ((W == nullptr) != (Z == nullptr)) return fail(SCOUP_EINVAL, "W and Z must both be given or both be NULL");
+    scoup_uplift* h = new scoup_uplift();
+    try {
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) {
+            delete h;
+            return fail(SCOUP_EINVAL, "bad device ordinal");
+        }
+        DeviceGuard dg(device);
+        h->device = device;
+        h->stream = (cudaStream_t)cuda_stream;
+        h->G = num_gaussians;
+        h->Npad = rows_padded;
+        h->L = L;
+        h->K = K;
+        CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+        if (W) {
+            h->W = W;
+            h->Z = Z;
+        } else {
+            CK(cudaMalloc((void**)&h->W, sizeof(float) * std::max<int64_t>(1, rows_padded) * L));
+            CK(cudaMalloc((void**)&h->Z, sizeof(float) * std::max<int64_t>(1, rows_padded)));
+            h->own_wz = true;
+        }
+        CK(cudaMalloc((void**)&h->d_err_code, sizeof(int)));
+        CK(cudaMalloc((void**)&h->d_err_index, sizeof(long long)));
+        CK(cudaMalloc((void**)&h->d_stats, 5 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
+        CK(cudaMemsetAsync(h->d_err_index, 0, sizeof(long long), h->stream));
+        CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * rows_padded * L, h->stream));
+        CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * rows_padded, h->stream));
+        const int64_t G = std::max<int64_t>(1, num_gaussians);
+        CK(cudaMalloc((void**)&h->pg.a, sizeof(float4) * G));
+        CK(cudaMalloc((void**)&h->pg.b, sizeof(float4) * G));
+        CK(cudaMalloc((void**)&h->pg.c, sizeof(float2) * G));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        for (int i = 0; i < 2; i++) {
+            CK(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
+            ctx_init(h->ctx[i]);
+        }
+        if (num_gaussians > 0) {
+            const float* src[4] = {means, scales, rotations, opacities};
+            const size_t cnt[4] = {3, 3, 4, 1};
+            const float* dsrc[4];
+            std::vector<float*> tmp;
+            for (int k = 0; k < 4; k++) {
+                if (is_device_ptr(src[k])) {
+                    dsrc[k] = src[k];
+                } else {
+                    float* d = nullptr;
+                    CK(cudaMalloc((void**)&d, sizeof(float) * cnt[k] * num_gaussians));
+                    CK(cudaMemcpyAsync(d, src[k], sizeof(float) * cnt[k] * num_gaussians, cudaMemcpyHostToDevice,
+                                       h->stream));
+                    tmp.push_back(d);
+                    dsrc[k] = d;
+                }
+            }
+            launch_activate(dsrc[0], dsrc[1], dsrc[2], dsrc[3], num_gaussians, h->pg, latch_of(h), h->stream);
+            CK(cudaGetLastError());
+            if (!tmp.empty()) {
+                CK(cudaStreamSynchronize(h->stream));
+                for (float* d : tmp) CK(cudaFree(d));
+            }
+        }
+    } catch (const CudaError& e) {
+        scoup_uplift_free(h);
+        return fail(e.err == cudaErrorMemoryAllocation ? SCOUP_ENOMEM : SCOUP_ECUDA,
+                    std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+    *out = h;
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const scoup_camera* cameras,
+                                    const uint32_t* region_ids, const int64_t* code_row0, const int32_t* num_regions,
+                                    const uint32_t* code_atoms, const float* code_coefs, int32_t S,
+                                    int64_t* contributions_out) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (h->latched) return fail(SCOUP_ESTATE, "a latched data error is pending; call scoup_uplift_reset");
+    if (num_views < 0) return fail(SCOUP_EINVAL, "num_views < 0");
+    if (num_views == 0) return SCOUP_OK;
+    if (!cameras || !region_ids || !code_row0 || !num_regions || !code_atoms || !code_coefs)
+        return fail(SCOUP_EINVAL, "NULL argument");
+    if (S < 1) return fail(SCOUP_EINVAL, "S < 1");
+    if (S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "S > SCOUP_MAX_S");
+    const int Wd = cameras[0].width, Hd = cameras[0].height;
+    int64_t rows = 0;
+    for (int v = 0; v < num_views; v++) {
+        const scoup_camera& c = cameras[v];
+        if (c.width != Wd || c.height != Hd) return fail(SCOUP_EINVAL, "cameras of one call must share width/height");
+        if (c.width <= 0 || c.height <= 0) return fail(SCOUP_EINVAL, "camera width/height <= 0");
+        if (!(c.fx > 0.f) || !(c.fy > 0.f) || !std::isfinite(c.fx) || !std::isfinite(c.fy) || !std::isfinite(c.cx) ||
+            !std::isfinite(c.cy))
+            return fail(SCOUP_EINVAL, "camera " + std::to_string(v) + ": bad intrinsics");
+        if (!rigid_ok(c.world_to_camera))
+            return fail(SCOUP_EDATA, "camera " + std::to_string(v) + ": world_to_camera is not rigid (1e-5)");
+        if (code_row0[v] < 0 || num_regions[v] < 0) return fail(SCOUP_EINVAL, "negative code_row0 / num_regions");
+        rows = std::max<int64_t>(rows, code_row0[v] + num_regions[v]);
+    }
+    if ((int64_t)Wd * Hd >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "image too large");
+    if (h->G == 0) return SCOUP_OK;
+    const int tiles_x = (Wd + TILE - 1) / TILE, tiles_y = (Hd + TILE - 1) / TILE;
+    const int64_t npx = (int64_t)Wd * Hd;
+    try {
+        DeviceGuard dg(h->device);
+        // ---- codes: copy (if host) + validate + truncate (Algorithm 1 per-pixel TopK)
+        if (rows > 0) {
+            const size_t nslots = (size_t)(rows * S);
+            if (nslots > h->code_cap) {
+                size_t cap = (size_t)((double)nslots * 1.25);
+                if (h->code_atoms) CK(cudaFree(h->code_atoms));
+                if (h->code_coefs) CK(cudaFree(h->code_coefs));
+                if (h->code_atoms_in) CK(cudaFree(h->code_atoms_in));
+                if (h->code_coefs_in) CK(cudaFree(h->code_coefs_in));
+                h->code_atoms = nullptr; h->code_coefs = nullptr; h->code_atoms_in = nullptr; h->code_coefs_in = nullptr;
+                h->code_cap = 0;
+                CK(cudaMalloc((void**)&h->code_atoms, sizeof(uint32_t) * cap));
+                CK(cudaMalloc((void**)&h->code_coefs, sizeof(float) * cap));
+                CK(cudaMalloc((void**)&h->code_atoms_in, sizeof(uint32_t) * cap));
+                CK(cudaMalloc((void**)&h->code_coefs_in, sizeof(float) * cap));
+                h->code_cap = cap;
+            }
+            const uint32_t* ain = code_atoms;
+            const float* cin = code_coefs;
+            if (!is_device_ptr(code_atoms) || !is_device_ptr(code_coefs)) {
+                CK(cudaMemcpyAsync(h->code_atoms_in, code_atoms, sizeof(uint32_t) * nslots, cudaMemcpyDefault, h->stream));
+                CK(cudaMemcpyAsync(h->code_coefs_in, code_coefs, sizeof(float) * nslots, cudaMemcpyDefault, h->stream));
+                ain = h->code_atoms_in;
+                cin = h->code_coefs_in;
+            }
+            launch_ingest_codes(ain, cin, rows, S, h->K, h->L, h->code_atoms, h->code_coefs, latch_of(h), h->stream);
+        }
+        const bool ids_on_device = is_device_ptr(region_ids);
+        // ---- fork the two view contexts off the caller's stream
+        CK(cudaEventRecord(h->ev_fork, h->stream));
+        for (int i = 0; i < 2; i++) {
+            CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
+            ctx_reserve_gaussians(h->ctx[i], h->G);
+        }
+        std::vector<Camera> cams(num_views);
+        for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
+        auto ids_for = [&](Ctx& c, int v) -> const uint32_t* {
+            if (ids_on_device) return region_ids + (int64_t)v * npx;
+            grow(&c.ids_stage, &c.ids_cap, (size_t)npx, 1.0);
+            CK(cudaMemcpyAsync(c.ids_stage, region_ids + (int64_t)v * npx, sizeof(uint32_t) * npx,
+                               cudaMemcpyHostToDevice, c.s));
+            return c.ids_stage;
+        };
+        scoup_status st = SCOUP_OK;
+        for (int v = 0; v <= num_views && st == SCOUP_OK; v++) {
+            if (v < num_views) {
+                Ctx& c = h->ctx[v & 1];
+                c.view = v;
+                c.ids_dev = ids_for(c, v);
+                stage1(h, c, cams[v], tiles_x, tiles_y);
+            }
+            if (v > 0) {
+                Ctx& c = h->ctx[(v - 1) & 1];
+                const int u = v - 1;
+                st = stage2(h, c, cams[u], tiles_x, tiles_y, c.ids_dev, code_row0[u], num_regions[u], S,
+                            contributions_out ? (long long*)contributions_out + u : nullptr, (long long)u * npx);
+            }
+        }
+        // ---- join back into the caller's stream
+        for (int i = 0; i < 2; i++) {
+            CK(cudaEventRecord(h->ev_join[i], h->ctx[i].s));
+            CK(cudaStreamWaitEvent(h->stream, h->ev_join[i], 0));
+        }
+        add_u64<<<1, 1, 0, h->stream>>>(h->d_stats + 0, (unsigned long long)num_views);
+        h->kernel_launches += 1 + (rows > 0 ? 1 : 0);
+        CK(cudaGetLastError());
+        if (st != SCOUP_OK) return st;
+    } catch (const CudaError& e) {
+        return fail(e.err == cudaErrorMemoryAllocation ? SCOUP_ENOMEM : SCOUP_ECUDA,
+                    std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_finalize_topk(scoup_uplift* h, int64_t first_row, int64_t num_rows, const float* W_rows,
+                                        const float* Z_rows, uint32_t* out_atoms, float* out_coefs) {
+    g_last_error.clear();
+    (void)Z_rows;
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (first_row < 0 || num_rows < 0) return fail(SCOUP_EINVAL, "negative row range");
+    if (num_rows > 0 && (!out_atoms || !out_coefs)) return fail(SCOUP_EINVAL, "NULL output");
+    if (!W_rows && first_row + num_rows > h->Npad) return fail(SCOUP_EINVAL, "row range beyond rows_padded");
+    try {
+        DeviceGuard dg(h->device);
+        if (num_rows > 0) {
+            const float* Wsrc = W_rows ? W_rows : h->W + first_row * (int64_t)h->L;
+            const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(num_rows, h->G - first_row));
+            const bool dev_out = is_device_ptr(out_atoms) && is_device_ptr(out_coefs);
+            uint32_t* da = out_atoms;
+            float* dc = out_coefs;
+            if (!dev_out) {
+                CK(cudaMalloc((void**)&da, sizeof(uint32_t) * num_rows * h->K));
+                CK(cudaMalloc((void**)&dc, sizeof(float) * num_rows * h->K));
+            }
+            if (h->timing) {
+                if (!h->topk_ev[0]) {
+                    CK(cudaEventCreate(&h->topk_ev[0]));
+                    CK(cudaEventCreate(&h->topk_ev[1]));
+                }
+                CK(cudaEventRecord(h->topk_ev[0], h->stream));
+            }
+            launch_topk(Wsrc, num_rows, valid, h->L, h->K, da, dc, h->stream);
+            h->kernel_launches += 1;
+            if (h->timing) {
+                CK(cudaEventRecord(h->topk_ev[1], h->stream));
+                CK(cudaEventSynchronize(h->topk_ev[1]));
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, h->topk_ev[0], h->topk_ev[1]));
+                h->t_topk += ms;
+            }
+            CK(cudaGetLastError());
+            if (!dev_out) {
+                CK(cudaMemcpyAsync(out_atoms, da, sizeof(uint32_t) * num_rows * h->K, cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(out_coefs, dc, sizeof(float) * num_rows * h->K, cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+                CK(cudaFree(da));
+                CK(cudaFree(dc));
+            }
+        }
+        CK(cudaStreamSynchronize(h->stream));
+        return check_latched(h);
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+}
+
+scoup_status scoup_uplift_reset(scoup_uplift* h) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    try {
+        DeviceGuard dg(h->device);
+        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * std::max<int64_t>(1, h->Npad) * h->L, h->stream));
+        CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * std::max<int64_t>(1, h->Npad), h->stream));
+        CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
+        h->latched = false;
+        h->host_entries = 0;
+        h->kernel_launches = 0;
+        h->cub_launches = 0;
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_get_accumulators(scoup_uplift* h, float** W, float** Z, int64_t* rows_padded) {
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (W) *W = h->W;
+    if (Z) *Z = h->Z;
+    if (rows_padded) *rows_padded = h->Npad;
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
+    g_last_error.clear();
+    if (!h || !out) return fail(SCOUP_EINVAL, "NULL argument");
+    try {
+        DeviceGuard dg(h->device);
+        unsigned long long s[5];
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpy(s, h->d_stats, sizeof(s), cudaMemcpyDeviceToHost));
+        out->views = (int64_t)s[0];
+        out->contributions = (int64_t)s[1];
+        out->tile_entries = h->host_entries;
+        out->visible = (int64_t)s[3];
+        out->support_tests = (int64_t)s[4];
+        out->kernel_launches = h->kernel_launches;
+        out->cub_launches = h->cub_launches;
+        return check_latched(h);
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+}
+
+scoup_status scoup_uplift_set_timing(scoup_uplift* h, int enable) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    try {
+        DeviceGuard dg(h->device);
+        for (int i = 0; i < 2; i++)
+            for (auto& es : h->ctx[i].evs) ev_accumulate(h, es);
+        h->timing = enable != 0;
+        h->t_pre = h->t_bin = h->t_ras = h->t_topk = 0;
+        h->ras_launches = h->views_timed = 0;
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_get_timing(scoup_uplift* h, scoup_timing* out) {
+    g_last_error.clear();
+    if (!h || !out) return fail(SCOUP_EINVAL, "NULL argument");
+    try {
+        DeviceGuard dg(h->device);
+        for (int i = 0; i < 2; i++)
+            for (auto& es : h->ctx[i].evs) ev_accumulate(h, es);
+        out->preprocess_ms = h->t_pre;
+        out->binning_ms = h->t_bin;
+        out->raster_ms = h->t_ras;
+        out->topk_ms = h->t_topk;
+        out->raster_launches = h->ras_launches;
+        out->views_timed = h->views_timed;
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+    return SCOUP_OK;
+}
+
+void scoup_uplift_free(scoup_uplift* h) {
+    if (!h) return;
+    DeviceGuard dg(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (int i = 0; i < 2; i++) {
+        if (h->ctx[i].s) cudaStreamSynchronize(h->ctx[i].s);
+        ctx_free(h->ctx[i]);
+        if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
+    }
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    for (int i = 0; i < 2; i++)
+        if (h->topk_ev[i]) cudaEventDestroy(h->topk_ev[i]);
+    void* ptrs[] = {h->pg.a, h->pg.b, h->pg.c, h->d_err_code, h->d_err_index, h->d_stats, h->code_atoms,
+                    h->code_coefs, h->code_atoms_in, h->code_coefs_in};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->own_wz) {
+        cudaFree(h->W);
+        cudaFree(h->Z);
+    }
+    delete h;
+}
+
+}  // extern "C"

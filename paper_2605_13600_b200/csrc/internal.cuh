@@ -1,0 +1,112 @@
+// internal.cuh -- shared declarations of the sm_100a CUDA path (not part of the C ABI).
+//
+// Parity-critical arithmetic is written with explicit round-to-nearest
+// intrinsics (__fmul_rn, __fadd_rn, __fdiv_rn, __fsqrt_rn, __fmaf_rn) so that no
+// compiler contraction or fast-math flag can change a rounding; the TU is also built
+// with -fmad=false.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace scoup {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr int TILE = 16;                 // 16x16 pixel tiles, one CTA (256 threads) each
+constexpr int TILE_PIX = TILE * TILE;
+constexpr int BATCH = 32;                // Gaussians staged per raster batch
+constexpr int MAX_SLOTS = 32;            // distinct regions per tile on the smem-aggregated path
+constexpr int MAX_S = 16;
+
+// DESIGN.md §3 constants (hex-exact fp32)
+#define K_NEAR 0x1.99999ap-3f
+#define K_LOWPASS 0x1.333334p-2f
+#define K_ACLAMP 0x1.fae148p-1f
+#define K_AMIN 0x1.010102p-8f
+#define K_TMIN 0x1.a36e2ep-14f
+#define K_HALF_LOG2E (-0x1.715476p-1f)
+#define K_LOG2E_NEG (-0x1.715476p+0f)
+
+struct Camera {
+    float fx, fy, cx, cy;
+    int width, height;
+    float P[12];  // rows of [R|t]
+};
+
+// Packed, activated Gaussians (derived once in init, DESIGN.md §3 G1).
+struct PackedGaussians {
+    float4* a;   // (mx, my, mz, o)   o < 0 marks an invalid Gaussian
+    float4* b;   // (V00, V01, V02, V11)
+    float2* c;   // (V12, V22)
+};
+
+// Per-view raster record, indexed by Gaussian id.
+//   rec0 = (mean2d.x, mean2d.y, r, o)     rec1 = (qa, qb, qc, ycut)
+struct ViewBuffers {
+    uint32_t* depth_key;     // [G] fp32 bits of t_z (visible) or 0xFFFFFFFF
+    uint32_t* depth_key_alt; // [G] sort scratch
+    uint32_t* gidx;          // [G] iota
+    uint32_t* gidx_sorted;   // [G] Gaussian ids in (depth, index) order
+    uint32_t* tiles;         // [G] tile count
+    uint64_t* offsets;       // [G] inclusive scan of tiles in depth order
+    uint2* rect;             // [G] (tx0 | ty0<<16, tx1 | ty1<<16)
+    float4* rec0;            // [G]
+    float4* rec1;            // [G]
+    uint32_t* ekey;          // [E] tile id of each (Gaussian, tile) entry
+    uint32_t* eval;          // [E] Gaussian id
+    uint32_t* ekey_alt;      // [E] sort scratch
+    uint32_t* eval_alt;      // [E]
+    uint2* ranges;           // [tiles] [begin, end) into the sorted entries
+};
+
+struct ErrorLatch {
+    int* code;         // device: 0 = none, else SCOUP_EDATA kind id
+    long long* index;  // device: first offending index
+};
+
+enum DataErr : int { ERR_NONE = 0, ERR_GAUSSIAN = 1, ERR_REGION = 2, ERR_CODE = 3 };
+
+__device__ __forceinline__ void latch_error(ErrorLatch e, int kind, long long idx) {
+    if (atomicCAS(e.code, 0, kind) == 0) *e.index = idx;
+}
+
+// ---- launchers (kernels.cu) ----
+void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
+                     int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);
+void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, int tiles_x, int tiles_y,
+                       ViewBuffers vb, unsigned long long* visible_ctr, cudaStream_t s);
+void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles, uint64_t* out,
+                              int64_t G, cudaStream_t s);
+void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, int tiles_x,
+                 int64_t G, uint32_t* ekey, uint32_t* eval, cudaStream_t s);
+void launch_ranges(const uint32_t* keys, int64_t E, uint2* ranges, cudaStream_t s);
+void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K,
+                         int L, uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s);
+
+struct RasterParams {
+    Camera cam;
+    int tiles_x, tiles_y;
+    const uint2* ranges;
+    const uint32_t* eval;
+    const float4* rec0;
+    const float4* rec1;
+    const uint32_t* region_ids;   // [H*W] this view
+    const uint32_t* code_atoms;   // sanitised table, rows of S slots
+    const float* code_coefs;
+    int64_t code_row0;
+    int32_t num_regions;
+    int S;
+    int L;
+    float* W;
+    float* Z;
+    unsigned long long* contrib_ctr;  // handle stats
+    unsigned long long* support_ctr;  // handle stats: support tests
+    long long* contrib_out;           // optional per-view output
+    ErrorLatch err;
+    long long pixel_base;             // for error indices
+};
+void launch_raster(const RasterParams& p, cudaStream_t s);
+
+void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                 float* coefs, cudaStream_t s);
+
+}  // namespace scoup

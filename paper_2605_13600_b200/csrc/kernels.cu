@@ -1,0 +1,435 @@
+// kernels.cu -- per-Gaussian, binning and finalize kernels of the sm_100a path.
+//
+//   activate        DESIGN.md §3 G1: q/|q|, R(q), Sigma_3D = R diag(s)^2 R^T
+//   preprocess      DESIGN.md §3 V1-V7: EWA projection, culls, support rect
+//   gather/emit     depth-ordered (Gaussian, tile) entries (3DGS tile binning)
+//   ranges          per-tile [begin, end) of the tile-sorted entries
+//   ingest_codes    Algorithm 1's per-pixel TopK(W_v(p)) realised per region
+//   topk            Eq. 6 Top-K + L1 renormalisation (Algorithm 1)
+#include "internal.cuh"
+
+namespace scoup {
+
+namespace {
+
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float dv(float a, float b) { return __fdiv_rn(a, b); }
+
+inline unsigned grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+// ------------------------------------------------------------------ activate (G1)
+__global__ void activate_kernel(const float* __restrict__ means, const float* __restrict__ scales,
+                                const float* __restrict__ rots, const float* __restrict__ opac,
+                                int64_t G, PackedGaussians pg, ErrorLatch err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G) return;
+    float mx = means[3 * i], my = means[3 * i + 1], mz = means[3 * i + 2];
+    float s0 = scales[3 * i], s1 = scales[3 * i + 1], s2 = scales[3 * i + 2];
+    float qw = rots[4 * i], qx = rots[4 * i + 1], qy = rots[4 * i + 2], qz = rots[4 * i + 3];
+    float o = opac[i];
+    bool ok = isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(qw) && isfinite(qx) &&
+              isfinite(qy) && isfinite(qz) && isfinite(s0) && isfinite(s1) && isfinite(s2) &&
+              s0 > 0.f && s1 > 0.f && s2 > 0.f && isfinite(o) && o >= 0.f && o <= 1.f;
+    float n = __fsqrt_rn(add(add(add(mul(qw, qw), mul(qx, qx)), mul(qy, qy)), mul(qz, qz)));
+    ok = ok && n > 0.f;
+    if (!ok) {
+        latch_error(err, ERR_GAUSSIAN, i);
+        pg.a[i] = make_float4(0.f, 0.f, 0.f, -1.f);
+        pg.b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        pg.c[i] = make_float2(0.f, 0.f);
+        return;
+    }
+    float w = dv(qw, n), x = dv(qx, n), y = dv(qy, n), z = dv(qz, n);
+    float R[3][3];
+    R[0][0] = sub(1.f, mul(2.f, add(mul(y, y), mul(z, z))));
+    R[0][1] = mul(2.f, sub(mul(x, y), mul(w, z)));
+    R[0][2] = mul(2.f, add(mul(x, z), mul(w, y)));
+    R[1][0] = mul(2.f, add(mul(x, y), mul(w, z)));
+    R[1][1] = sub(1.f, mul(2.f, add(mul(x, x), mul(z, z))));
+    R[1][2] = mul(2.f, sub(mul(y, z), mul(w, x)));
+    R[2][0] = mul(2.f, sub(mul(x, z), mul(w, y)));
+    R[2][1] = mul(2.f, add(mul(y, z), mul(w, x)));
+    R[2][2] = sub(1.f, mul(2.f, add(mul(x, x), mul(y, y))));
+    const float s[3] = {s0, s1, s2};
+    float M[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) M[a][b] = mul(R[a][b], s[b]);
+    float V[6];
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = a; b < 3; b++)
+            V[k++] = add(add(mul(M[a][0], M[b][0]), mul(M[a][1], M[b][1])), mul(M[a][2], M[b][2]));
+    pg.a[i] = make_float4(mx, my, mz, o);
+    pg.b[i] = make_float4(V[0], V[1], V[2], V[3]);
+    pg.c[i] = make_float2(V[4], V[5]);
+}
+
+// ------------------------------------------------------------------ preprocess (V1-V7)
+__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, Camera cam,
+                                                         int tiles_x, int tiles_y, ViewBuffers vb,
+                                                         unsigned long long* visible_ctr) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool vis = false;
+    if (i < G) {
+        float4 A = pg.a[i];
+        uint32_t key = NONE, ntiles = 0;
+        const float o = A.w;
+        // V1: camera-space mean
+        float t[3];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+            t[a] = add(add(add(mul(cam.P[4 * a + 0], A.x), mul(cam.P[4 * a + 1], A.y)),
+                           mul(cam.P[4 * a + 2], A.z)),
+                       cam.P[4 * a + 3]);
+        // V2: near plane; exact opacity cull (alpha <= o < 1/255 never contributes)
+        if (t[2] > K_NEAR && o >= K_AMIN) {
+            float4 B = pg.b[i];
+            float2 Cc = pg.c[i];
+            const float Vm[3][3] = {{B.x, B.y, B.z}, {B.y, B.w, Cc.x}, {B.z, Cc.x, Cc.y}};
+            // V3
+            float u = dv(t[0], t[2]), v = dv(t[1], t[2]);
+            float mx = add(mul(cam.fx, u), cam.cx);
+            float my = add(mul(cam.fy, v), cam.cy);
+            float j00 = dv(cam.fx, t[2]);
+            float j02 = dv(-mul(cam.fx, u), t[2]);
+            float j11 = dv(cam.fy, t[2]);
+            float j12 = dv(-mul(cam.fy, v), t[2]);
+            // V4: Q = J W
+            float Q[2][3];
+#pragma unroll
+            for (int b = 0; b < 3; b++) {
+                Q[0][b] = add(mul(j00, cam.P[0 * 4 + b]), mul(j02, cam.P[2 * 4 + b]));
+                Q[1][b] = add(mul(j11, cam.P[1 * 4 + b]), mul(j12, cam.P[2 * 4 + b]));
+            }
+            // V5: U = Q Sigma_3D;  Sigma_2D = U Q^T + 0.3 I
+            float U[2][3];
+#pragma unroll
+            for (int a = 0; a < 2; a++)
+#pragma unroll
+                for (int b = 0; b < 3; b++)
+                    U[a][b] = add(add(mul(Q[a][0], Vm[0][b]), mul(Q[a][1], Vm[1][b])), mul(Q[a][2], Vm[2][b]));
+            float sxx = add(add(add(mul(U[0][0], Q[0][0]), mul(U[0][1], Q[0][1])), mul(U[0][2], Q[0][2])), K_LOWPASS);
+            float sxy = add(add(mul(U[0][0], Q[1][0]), mul(U[0][1], Q[1][1])), mul(U[0][2], Q[1][2]));
+            float syy = add(add(add(mul(U[1][0], Q[1][0]), mul(U[1][1], Q[1][1])), mul(U[1][2], Q[1][2])), K_LOWPASS);
+            // V6: conic
+            float det = sub(mul(sxx, syy), mul(sxy, sxy));
+            if (det > 0.f) {
+                float ca = dv(syy, det), cb = dv(-sxy, det), cc = dv(sxx, det);
+                // V7: radius of the square support
+                float mid = mul(0.5f, add(sxx, syy));
+                float lam = add(mid, __fsqrt_rn(fmaxf(0.f, sub(mul(mid, mid), det))));
+                float r = mul(3.f, __fsqrt_rn(lam));
+                float qa = mul(ca, K_HALF_LOG2E), qb = mul(cb, K_LOG2E_NEG), qc = mul(cc, K_HALF_LOG2E);
+                // GPU-only conservative prune (not part of the spec):
+                // y < ycut  =>  o * exp2_spec(y) < 1/255 with a 0.7% margin.
+                float ycut = -log2f(255.f * o) - 0.01f;
+                // support = square |d| <= r intersected with the bbox of the alpha >= 1/255
+                // ellipse d^T conic d <= m^2, m^2 = -2 ln2 ycut.  The bbox half-widths are
+                // m sqrt((conic^-1)_xx), taken from the conic actually evaluated (fp64, so
+                // an ill-conditioned det cannot shrink it) and padded; exact test per pixel.
+                float hx = r, hy = r;
+                {
+                    double dca = ca, dcb = cb, dcc = cc;
+                    double detc = dca * dcc - dcb * dcb;
+                    double m2 = -2.0 * 0.6931471805599453 * (double)ycut;
+                    if (detc > 0.0 && m2 > 0.0) {
+                        double ex = sqrt(m2 * dcc / detc) * 1.001 + 0.01;
+                        double ey = sqrt(m2 * dca / detc) * 1.001 + 0.01;
+                        hx = (float)fmin((double)r, ex);
+                        hy = (float)fmin((double)r, ey);
+                    }
+                }
+                float padx = 1.0f + 1e-6f * (fabsf(mx) + hx);
+                float pady = 1.0f + 1e-6f * (fabsf(my) + hy);
+                float fx0 = floorf(mx - hx - 0.5f - padx), fx1 = ceilf(mx + hx - 0.5f + padx);
+                float fy0 = floorf(my - hy - 0.5f - pady), fy1 = ceilf(my + hy - 0.5f + pady);
+                const float Wm1 = (float)(cam.width - 1), Hm1 = (float)(cam.height - 1);
+                bool finite = isfinite(mx) && isfinite(my) && isfinite(r) && isfinite(qa) && isfinite(qb) && isfinite(qc);
+                if (finite && fx1 >= 0.f && fx0 <= Wm1 && fy1 >= 0.f && fy0 <= Hm1) {
+                    int x0 = (int)fmaxf(fx0, 0.f), x1 = (int)fminf(fx1, Wm1);
+                    int y0 = (int)fmaxf(fy0, 0.f), y1 = (int)fminf(fy1, Hm1);
+                    int tx0 = x0 / TILE, tx1 = x1 / TILE + 1, ty0 = y0 / TILE, ty1 = y1 / TILE + 1;
+                    ntiles = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
+                    key = __float_as_uint(t[2]);
+                    vb.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
+                    vb.rec0[i] = make_float4(mx, my, r, o);
+                    vb.rec1[i] = make_float4(qa, qb, qc, ycut);
+                    vis = true;
+                }
+            }
+        }
+        vb.depth_key[i] = key;
+        vb.tiles[i] = ntiles;
+        vb.gidx[i] = (uint32_t)i;
+    }
+    unsigned ballot = __ballot_sync(0xffffffffu, vis);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(visible_ctr, (unsigned long long)__popc(ballot));
+}
+
+__global__ void gather_tiles_kernel(const uint32_t* __restrict__ gidx_sorted, const uint32_t* __restrict__ tiles,
+                                    uint64_t* __restrict__ out, int64_t G) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < G) out[k] = tiles[gidx_sorted[k]];
+}
+
+// ------------------------------------------------------------------ emit
+// Entry m of the Gaussian at depth position k goes to slot offsets[k-1] + m, so the
+// entries are in (depth, index) order before the stable tile sort.
+__device__ __forceinline__ void emit_range(uint32_t g, uint2 rect, int tiles_x, uint64_t off, uint32_t m0,
+                                           uint32_t m1, uint32_t* ekey, uint32_t* eval) {
+    uint32_t tx0 = rect.x & 0xFFFFu, ty0 = rect.x >> 16, tx1 = rect.y & 0xFFFFu;
+    uint32_t w = tx1 - tx0;
+    for (uint32_t m = m0; m < m1; m++) {
+        uint32_t ty = ty0 + m / w, tx = tx0 + m % w;
+        ekey[off + m] = ty * (uint32_t)tiles_x + tx;
+        eval[off + m] = g;
+    }
+}
+
+__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ gidx_sorted,
+                                                   const uint64_t* __restrict__ offsets,
+                                                   const uint2* __restrict__ rect, int tiles_x, int64_t G,
+                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t begin = 0, end = 0;
+    uint32_t g = 0;
+    uint2 rc = make_uint2(0, 0);
+    if (k < G) {
+        begin = k > 0 ? offsets[k - 1] : 0;
+        end = offsets[k];
+        if (end > begin) {
+            g = gidx_sorted[k];
+            rc = rect[g];
+        }
+    }
+    uint32_t cnt = (uint32_t)(end - begin);
+    const uint32_t SMALL = 8;
+    if (cnt > 0 && cnt <= SMALL) emit_range(g, rc, tiles_x, begin, 0, cnt, ekey, eval);
+    unsigned big = __ballot_sync(0xffffffffu, cnt > SMALL);
+    while (big) {
+        int src = __ffs(big) - 1;
+        big &= big - 1;
+        uint32_t sg = __shfl_sync(0xffffffffu, g, src);
+        uint32_t rx = __shfl_sync(0xffffffffu, rc.x, src), ry = __shfl_sync(0xffffffffu, rc.y, src);
+        uint64_t sb = __shfl_sync(0xffffffffu, begin, src);
+        uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
+        uint32_t tx0 = rx & 0xFFFFu, ty0 = rx >> 16, w = (ry & 0xFFFFu) - tx0;
+        for (uint32_t m = lane; m < sc; m += 32) {
+            uint32_t ty = ty0 + m / w, tx = tx0 + m % w;
+            ekey[sb + m] = ty * (uint32_t)tiles_x + tx;
+            eval[sb + m] = sg;
+        }
+    }
+}
+
+__global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t E, uint2* __restrict__ ranges) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E) return;
+    uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == E - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+}
+
+// ------------------------------------------------------------------ ingest codes
+// Validate each region code and truncate it to its K largest slots (ties -> lower atom),
+// Algorithm 1's per-pixel TopK(W_v(p)).  No renormalisation.
+__global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const float* __restrict__ coefs_in,
+                                    int64_t rows, int S, int K, int L, uint32_t* __restrict__ atoms_out,
+                                    float* __restrict__ coefs_out, ErrorLatch err) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    uint32_t a[MAX_S];
+    float c[MAX_S];
+    for (int s = 0; s < S; s++) {
+        a[s] = atoms_in[r * S + s];
+        c[s] = coefs_in[r * S + s];
+        if (a[s] != NONE && (a[s] >= (uint32_t)L || !isfinite(c[s]) || c[s] < 0.f)) {
+            latch_error(err, ERR_CODE, r * S + s);
+            a[s] = NONE;
+            c[s] = 0.f;
+        }
+    }
+    if (S > K) {
+        for (int kept = 0; kept < K; kept++) {
+            int best = -1;
+            for (int s = kept; s < S; s++) {
+                if (a[s] == NONE) continue;
+                if (best < 0 || c[s] > c[best] || (c[s] == c[best] && a[s] < a[best])) best = s;
+            }
+            if (best < 0) break;
+            uint32_t ta = a[kept]; float tc = c[kept];
+            a[kept] = a[best]; c[kept] = c[best];
+            a[best] = ta; c[best] = tc;
+        }
+        for (int s = K; s < S; s++) { a[s] = NONE; c[s] = 0.f; }
+    }
+    for (int s = 0; s < S; s++) {
+        atoms_out[r * S + s] = a[s];
+        coefs_out[r * S + s] = c[s];
+    }
+}
+
+// ------------------------------------------------------------------ Top-K (Eq. 6)
+// One thread per Gaussian row.  The KMAX best (value, atom) pairs live in registers,
+// ordered (value desc, atom asc); a new value bubbles in only if strictly larger than the
+// current KMAX-th, so equal values keep the lower atom (atoms are scanned ascending).
+// Only positive values enter (registers start at 0).  Z_i cancels in the L1
+// renormalisation, so selection runs on the raw sums.
+template <int KMAX>
+__global__ void __launch_bounds__(128) topk_kernel(const float* __restrict__ W, int64_t rows, int64_t valid_rows,
+                                                   int L, int K, uint32_t* __restrict__ atoms,
+                                                   float* __restrict__ coefs) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float bv[KMAX];
+    uint32_t ba[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
+    if (r < valid_rows) {
+        const float4* row = reinterpret_cast<const float4*>(W + r * (int64_t)L);
+        for (int c4 = 0; c4 < L / 4; c4++) {
+            float4 v4 = __ldg(row + c4);
+            float vals[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                float v = vals[u];
+                if (v > bv[KMAX - 1]) {
+                    uint32_t a = (uint32_t)(c4 * 4 + u);
+#pragma unroll
+                    for (int s = 0; s < KMAX; s++) {
+                        bool sw = v > bv[s];
+                        float tv = sw ? bv[s] : v;
+                        uint32_t ta = sw ? ba[s] : a;
+                        bv[s] = sw ? v : bv[s];
+                        ba[s] = sw ? a : ba[s];
+                        v = tv;
+                        a = ta;
+                    }
+                }
+            }
+        }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int s = 0; s < KMAX; s++)
+        if (s < K) sum = __fadd_rn(sum, bv[s]);
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) {
+        if (s < K) {
+            bool keep = bv[s] > 0.f;
+            atoms[r * K + s] = keep ? ba[s] : NONE;
+            coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+        }
+    }
+}
+
+// generic L (not a multiple of 4): scalar loads
+template <int KMAX>
+__global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restrict__ W, int64_t rows,
+                                                          int64_t valid_rows, int L, int K,
+                                                          uint32_t* __restrict__ atoms, float* __restrict__ coefs) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float bv[KMAX];
+    uint32_t ba[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
+    if (r < valid_rows) {
+        for (int c = 0; c < L; c++) {
+            float v = __ldg(W + r * (int64_t)L + c);
+            if (v > bv[KMAX - 1]) {
+                uint32_t a = (uint32_t)c;
+#pragma unroll
+                for (int s = 0; s < KMAX; s++) {
+                    bool sw = v > bv[s];
+                    float tv = sw ? bv[s] : v;
+                    uint32_t ta = sw ? ba[s] : a;
+                    bv[s] = sw ? v : bv[s];
+                    ba[s] = sw ? a : ba[s];
+                    v = tv;
+                    a = ta;
+                }
+            }
+        }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int s = 0; s < KMAX; s++)
+        if (s < K) sum = __fadd_rn(sum, bv[s]);
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) {
+        if (s < K) {
+            bool keep = bv[s] > 0.f;
+            atoms[r * K + s] = keep ? ba[s] : NONE;
+            coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+        }
+    }
+}
+
+}  // namespace
+
+void launch_activate(const float* means, const float* scales, const float* rots, const float* opac, int64_t G,
+                     PackedGaussians pg, ErrorLatch err, cudaStream_t s) {
+    if (G <= 0) return;
+    activate_kernel<<<grid_for(G, 256), 256, 0, s>>>(means, scales, rots, opac, G, pg, err);
+}
+
+void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, int tiles_x, int tiles_y, ViewBuffers vb,
+                       unsigned long long* visible_ctr, cudaStream_t s) {
+    if (G <= 0) return;
+    preprocess_kernel<<<grid_for(G, 256), 256, 0, s>>>(pg, G, cam, tiles_x, tiles_y, vb, visible_ctr);
+}
+
+void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles, uint64_t* out, int64_t G,
+                              cudaStream_t s) {
+    if (G <= 0) return;
+    gather_tiles_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, tiles, out, G);
+}
+
+void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, int tiles_x, int64_t G,
+                 uint32_t* ekey, uint32_t* eval, cudaStream_t s) {
+    if (G <= 0) return;
+    emit_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, offsets, rect, tiles_x, G, ekey, eval);
+}
+
+void launch_ranges(const uint32_t* keys, int64_t E, uint2* ranges, cudaStream_t s) {
+    if (E <= 0) return;
+    ranges_kernel<<<grid_for(E, 256), 256, 0, s>>>(keys, E, ranges);
+}
+
+void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K, int L,
+                         uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s) {
+    if (rows <= 0) return;
+    ingest_codes_kernel<<<grid_for(rows, 128), 128, 0, s>>>(atoms_in, coefs_in, rows, S, K, L, atoms_out,
+                                                            coefs_out, err);
+}
+
+template <int KMAX>
+static void topk_dispatch(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                          float* coefs, cudaStream_t s) {
+    if (L % 4 == 0 && (reinterpret_cast<uintptr_t>(W) % 16) == 0)
+        topk_kernel<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs);
+    else
+        topk_kernel_scalar<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs);
+}
+
+void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms, float* coefs,
+                 cudaStream_t s) {
+    if (rows <= 0) return;
+    if (K <= 4) topk_dispatch<4>(W, rows, valid_rows, L, K, atoms, coefs, s);
+    else if (K <= 8) topk_dispatch<8>(W, rows, valid_rows, L, K, atoms, coefs, s);
+    else if (K <= 16) topk_dispatch<16>(W, rows, valid_rows, L, K, atoms, coefs, s);
+    else topk_dispatch<32>(W, rows, valid_rows, L, K, atoms, coefs, s);
+}
+
+}  // namespace scoup

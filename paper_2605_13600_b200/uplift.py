@@ -1,0 +1,101 @@
+"""User-facing Python API over the C ABI (torch tensors for device memory and streams).
+
+    up = SparseUplift(gaussians, L=64, K=4)          # scoup_uplift_init
+    up.add_views(cameras, region_ids, codes)         # scoup_uplift_add_views  (Eq. 5)
+    atoms, coefs = up.finalize()                     # scoup_uplift_finalize_topk (Eq. 6)
+
+PyTorch only provides device memory (the W/Z accumulators are torch tensors so they can
+feed `torch.distributed.reduce_scatter_tensor` directly) and the current CUDA stream.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import abi
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class SparseUplift:
+    """One semantic level's uplift on one device (Algorithm 1)."""
+
+    def __init__(self, gaussians, L: int, K: int, device: int = 0, rows_padded: int = 0,
+                 stream=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("SparseUplift needs a CUDA device (there is no CPU fallback)")
+        self.device = torch.device("cuda", device)
+        self.L, self.K = int(L), int(K)
+        G = int(gaussians.means.shape[0])
+        self.G = G
+        self.rows_padded = int(rows_padded) if rows_padded else G
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.W = torch.empty((max(1, self.rows_padded), self.L), dtype=torch.float32, device=self.device)
+        self.Z = torch.empty((max(1, self.rows_padded),), dtype=torch.float32, device=self.device)
+        keep = [self._as_input(a) for a in (gaussians.means, gaussians.scales, gaussians.rotations,
+                                            gaussians.opacities)]
+        self._h = abi.scoup_uplift_init(device, self.stream.cuda_stream, G, *keep, self.L, self.K,
+                                        self.W, self.Z, self.rows_padded)
+        self._keep = keep  # device inputs must outlive the stream point of init
+
+    def _as_input(self, a):
+        torch = _torch()
+        if isinstance(a, np.ndarray):
+            return np.ascontiguousarray(a, dtype=np.float32)
+        return a.contiguous()
+
+    def add_views(self, cameras: Sequence, region_ids, codes, contributions_out=None):
+        """region_ids: [V,H,W] uint32 numpy (host) or int32/uint32 torch tensor (device or host).
+        codes: synth.Codes-like (atoms [rows,S] u32, coefs [rows,S] f32, row0 [V], num_regions [V])."""
+        atoms = codes.atoms if not isinstance(codes.atoms, np.ndarray) else np.ascontiguousarray(codes.atoms, np.uint32)
+        coefs = codes.coefs if not isinstance(codes.coefs, np.ndarray) else np.ascontiguousarray(codes.coefs, np.float32)
+        S = int(atoms.shape[1])
+        abi.scoup_uplift_add_views(self._h, list(cameras), region_ids, codes.row0, codes.num_regions,
+                                   atoms, coefs, S, contributions_out)
+
+    def finalize(self, first_row: int = 0, num_rows: Optional[int] = None, W_rows=None, Z_rows=None,
+                 out_atoms=None, out_coefs=None):
+        """Eq. 6 on rows [first_row, first_row+num_rows).  Returns (atoms u32->int32 view, coefs)."""
+        torch = _torch()
+        if num_rows is None:
+            num_rows = (W_rows.shape[0] if W_rows is not None else self.G - first_row)
+        if out_atoms is None:
+            out_atoms = torch.empty((num_rows, self.K), dtype=torch.int32, device=self.device)
+        if out_coefs is None:
+            out_coefs = torch.empty((num_rows, self.K), dtype=torch.float32, device=self.device)
+        abi.scoup_uplift_finalize_topk(self._h, first_row, num_rows, W_rows, Z_rows, out_atoms, out_coefs)
+        return out_atoms, out_coefs
+
+    def reset(self):
+        abi.scoup_uplift_reset(self._h)
+
+    def stats(self) -> dict:
+        return abi.scoup_uplift_get_stats(self._h)
+
+    def set_timing(self, enable: bool = True):
+        abi.scoup_uplift_set_timing(self._h, enable)
+
+    def timing(self) -> dict:
+        return abi.scoup_uplift_get_timing(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            abi.scoup_uplift_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): W and Z within 1e-4 relative / 1e-6 absolute element by
+element; per-view contribution counts bit-exact (the fragment weights are bit-identical by
+DESIGN.md §3, so a single flipped threshold decision fails the count); Top-K codes equal
+except among near-ties of the K-th value (tests/helpers.compare_codes).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2605_13600_b200 import synth
+from helpers import NONE, compare_accumulators, compare_codes, full_frame_codes, gaussians, identity_camera
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-6
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_13600_b200 import build
+    build.build()
+    return torch.device("cuda", 0)
+
+
+def run_gpu(g, cams, maps, codes, L, K, *, host_inputs=False, split=None, rows_padded=0):
+    from paper_2605_13600_b200.uplift import SparseUplift
+    V = len(cams)
+    if host_inputs:
+        gin = g
+        ids = np.ascontiguousarray(maps, np.uint32)
+        cod = codes
+    else:
+        gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                                for a in (g.means, g.scales, g.rotations, g.opacities)])
+        ids = torch.from_numpy(np.ascontiguousarray(maps).view(np.int32)).cuda()
+        cod = synth.Codes(torch.from_numpy(np.ascontiguousarray(codes.atoms).view(np.int32)).cuda(),
+                          torch.from_numpy(np.ascontiguousarray(codes.coefs)).cuda(), codes.row0, codes.num_regions)
+    contrib = torch.zeros(V, dtype=torch.int64, device="cuda")
+    up = SparseUplift(gin, L, K, rows_padded=rows_padded)
+    try:
+        chunks = [list(range(V))] if split is None else split
+        for ch in chunks:
+            sub_ids = ids[ch] if not host_inputs else np.ascontiguousarray(ids[ch])
+            sub_codes = synth.Codes(cod.atoms, cod.coefs, codes.row0[ch], codes.num_regions[ch])
+            out = contrib[ch[0]:ch[-1] + 1] if ch == list(range(ch[0], ch[-1] + 1)) else None
+            up.add_views([cams[v] for v in ch], sub_ids.contiguous() if not host_inputs else sub_ids, sub_codes,
+                         contributions_out=out)
+        atoms, coefs = up.finalize()
+        torch.cuda.synchronize()
+        W = up.W[:g.count].double().cpu().numpy()
+        Z = up.Z[:g.count].double().cpu().numpy()
+        st = up.stats()
+        return dict(W=W, Z=Z, atoms=atoms.cpu().numpy().view(np.uint32), coefs=coefs.cpu().numpy(),
+                    contrib=contrib.cpu().numpy(), stats=st)
+    finally:
+        up.close()
+
+
+def assert_parity(res, ora, K, check_counts=True):
+    W, Z, frags, oatoms, ocoefs = ora
+    bad_w, bad_z = compare_accumulators(res["W"], res["Z"], W, Z, RTOL, ATOL)
+    assert len(bad_w) == 0, f"{len(bad_w)} W mismatches, first {bad_w[:3]}: gpu {res['W'][tuple(bad_w[0])]} ora {W[tuple(bad_w[0])]}"
+    assert len(bad_z) == 0, f"{len(bad_z)} Z mismatches, first {bad_z[:3]}"
+    if check_counts:
+        assert res["contrib"].tolist() == frags.tolist()
+        assert res["stats"]["contributions"] == int(frags.sum())
+    bad, ties, worst = compare_codes(res["atoms"], res["coefs"], W, K, RTOL, ATOL)
+    assert bad == 0, worst
+    return ties
+
+
+def test_tiny_full_parity(dev, tiny_scene, tiny_oracle):
+    cfg, scene, maps, codes = tiny_scene
+    res = run_gpu(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    assert_parity(res, tiny_oracle, cfg.K)
+
+
+def test_tiny_host_buffers_match_device_buffers(dev, tiny_scene, tiny_oracle):
+    """The C ABI accepts host arrays (copied inside the call): same results."""
+    cfg, scene, maps, codes = tiny_scene
+    res = run_gpu(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, host_inputs=True)
+    assert_parity(res, tiny_oracle, cfg.K)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_tiny_other_seeds_with_unassigned(dev, seed):
+    """Seeds 1-3; 10% of regions unassigned (NONE pixels add to Z only)."""
+    cfg = synth.CONFIGS["tiny"].with_(unassigned_frac=0.1)
+    scene = synth.make_scene(cfg, seed)
+    maps = synth.make_region_maps_numpy(cfg, seed=seed)
+    codes = synth.make_codes(cfg, seed=seed)
+    assert (maps == NONE).any()
+    ora = oracle.uplift(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    res = run_gpu(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    assert_parity(res, ora, cfg.K)
+
+
+def test_streaming_add_views_equals_one_call(dev, tiny_scene, tiny_oracle):
+    """add_views may be called repeatedly (checkpoint-friendly accumulation)."""
+    cfg, scene, maps, codes = tiny_scene
+    res = run_gpu(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, split=[[0], [1, 2], [3]])
+    assert_parity(res, tiny_oracle, cfg.K)
+
+
+def test_small_config_view_subset(dev):
+    """configs[1] (100k clustered Gaussians, 512x384, 64 regions) on 6 of its 50 views."""
+    cfg = synth.CONFIGS["small"]
+    scene = synth.make_scene(cfg, 0)
+    views = [0, 9, 17, 25, 33, 41]
+    maps = synth.make_region_maps_numpy(cfg, seed=0, views=views)
+    codes = synth.make_codes(cfg, seed=0, views=views)
+    cams = [scene.cameras[v] for v in views]
+    ora = oracle.uplift(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    ties = assert_parity(res, ora, cfg.K)
+    assert ties < 0.01 * scene.gaussians.count
+
+
+def test_ragged_image_and_many_regions_fallback(dev):
+    """Image 70x45 (ragged tiles on both axes) and a region map of per-pixel noise: tiles hold
+    more than MAX_SLOTS distinct regions, exercising the per-pixel reduction path."""
+    rng = np.random.default_rng(11)
+    G = 3000
+    g = gaussians(rng.uniform(-1, 1, (G, 3)), np.exp(rng.normal(np.log(0.04), 0.5, (G, 3))),
+                  rng.normal(size=(G, 4)), 1 / (1 + np.exp(-rng.normal(0, 1.5, G))))
+    cams = [synth.look_at_camera(np.array(p) * 3.0, 70, 45, 60.0) for p in
+            ([1, 0.2, 0.3], [-0.3, 1, 0.1], [0.2, -0.5, 1])]
+    R = 300
+    maps = rng.integers(0, R, size=(3, 45, 70)).astype(np.uint32)
+    maps[1, :, :35] = rng.integers(0, 3, size=(45, 35))  # half the view few regions
+    maps[2, 10:20, 10:20] = NONE
+    codes = synth.make_codes(synth.CONFIGS["tiny"].with_(num_views=3, regions=(R,)), seed=4)
+    ora = oracle.uplift(g, cams, maps, codes, 64, 4)
+    res = run_gpu(g, cams, maps, codes, 64, 4)
+    assert_parity(res, ora, 4)
+
+
+@pytest.mark.parametrize("L,K,S", [(16, 1, 4), (63, 5, 3), (32, 16, 6), (128, 8, 12)])
+def test_code_shapes_and_truncation(dev, tiny_scene, L, K, S):
+    """L not a multiple of 4 (scalar Top-K loads), K = 1 and K = 16, S > K codes (Algorithm 1
+    per-pixel TopK truncation), L = 128 (stress config)."""
+    cfg, scene, maps, _ = tiny_scene
+    c2 = cfg.with_(L=L, S=S, K=K)
+    codes = synth.make_codes(c2, seed=5)
+    cams = scene.cameras[:2]
+    ora = oracle.uplift(scene.gaussians, cams, maps[:2], codes, L, K)
+    res = run_gpu(scene.gaussians, cams, maps[:2], codes, L, K)
+    assert_parity(res, ora, K)
+
+
+def test_edge_cases_empty_and_culled(dev):
+    """No Gaussian visible (all behind the camera), a single Gaussian, and padded rows."""
+    cam = identity_camera(40, 30, 50.0)
+    g = gaussians([[0, 0, -2], [0.1, 0, -3]], np.full((2, 3), 0.1), np.tile([1, 0, 0, 0], (2, 1)), [0.5, 0.9])
+    codes = full_frame_codes([[(1, 1.0)]])
+    ids = np.zeros((1, 30, 40), np.uint32)
+    res = run_gpu(g, [cam], ids, codes, 8, 2, rows_padded=5)
+    assert res["stats"]["contributions"] == 0 and np.all(res["W"] == 0) and np.all(res["Z"] == 0)
+    assert np.all(res["atoms"] == NONE) and np.all(res["coefs"] == 0)
+    g1 = gaussians([[0, 0, 2]], [[0.1, 0.05, 0.1]], [[1, 0.2, 0, 0]], [0.7])
+    ora = oracle.uplift(g1, [cam], ids, codes, 8, 2)
+    res = run_gpu(g1, [cam], ids, codes, 8, 2, rows_padded=4)
+    assert_parity(res, ora, 2)
+
+
+def test_closed_form_cases_on_gpu(dev):
+    """F3/F4 on the GPU path: exact e values at the centre pixel (alpha = 0.5 -> 0.5, 0.25) and the
+    termination reading, visible through W with a per-pixel one-hot region code."""
+    cam = identity_camera(96, 96, 100.0, 48.5, 48.5)
+    g = gaussians([[0, 0, 2], [0, 0, 3], [0, 0, 4]], np.full((3, 3), 0.2), np.tile([1, 0, 0, 0], (3, 1)),
+                  [0.99, 0.99, 0.99])
+    ids = np.full((1, 96, 96), 1, np.uint32)
+    ids[0, 48, 48] = 0
+    codes = synth.Codes(np.array([[5], [6]], np.uint32), np.array([[1.0], [1.0]], np.float32),
+                        np.array([0], np.int64), np.array([2], np.int32))
+    res = run_gpu(g, [cam], ids, codes, 8, 2)
+    assert res["W"][0, 5] == np.float32(0.99)
+    assert res["W"][1, 5] == 0.0 and res["W"][2, 5] == 0.0
+    ora = oracle.uplift(g, [cam], ids, codes, 8, 2)
+    assert_parity(res, ora, 2)
+
+
+def test_data_errors_are_latched(dev, tiny_scene):
+    """Region id >= R_v and atom >= L are data errors, reported at the next
+    synchronising call with the offending index; reset clears them."""
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    bad = maps[:1].copy()
+    bad[0, 10, 20] = 999
+    up = SparseUplift(scene.gaussians, cfg.L, cfg.K)
+    try:
+        up.add_views(scene.cameras[:1], bad, codes)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.finalize()
+        assert ei.value.status == 2 and str(10 * 64 + 20) in str(ei.value)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.add_views(scene.cameras[:1], maps[:1], codes)
+        assert ei.value.status == 5
+        up.reset()
+        bad_codes = synth.Codes(codes.atoms.copy(), codes.coefs, codes.row0, codes.num_regions)
+        bad_codes.atoms[3, 1] = 64
+        up.add_views(scene.cameras[:1], maps[:1], bad_codes)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.finalize()
+        assert ei.value.status == 2 and str(3 * 4 + 1) in str(ei.value)
+        up.reset()
+        cam = scene.cameras[0]
+        skew = synth.Camera(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                            cam.world_to_camera * np.float32(1.01))
+        with pytest.raises(abi.ScoupError) as ei:
+            up.add_views([skew], maps[:1], codes)
+        assert ei.value.status == 2
+    finally:
+        up.close()
+    with pytest.raises(abi.ScoupError) as ei:
+        SparseUplift(scene.gaussians, 8, 9)
+    assert ei.value.status == 1
+
+
+def test_nonfinite_gaussian_latched(dev, tiny_scene):
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    g = scene.gaussians
+    m = g.means.copy()
+    m[17, 1] = np.nan
+    up = SparseUplift(synth.Gaussians(m, g.scales, g.rotations, g.opacities), cfg.L, cfg.K)
+    try:
+        up.add_views(scene.cameras[:1], maps[:1], codes)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.finalize()
+        assert ei.value.status == 2 and "17" in str(ei.value)
+    finally:
+        up.close()
+
+
+def test_outdoor_full_size_sampled_views(dev):
+    """configs[3] at full size (3M Gaussians, 1600x1066, L=64, S=K=8) in the launch configuration
+    bench.py times, on 2 sampled views the oracle can compute: element-wise W/Z parity over all
+    3M rows, exact per-view contribution counts, and Top-K code parity."""
+    cfg = synth.CONFIGS["outdoor"]
+    scene = synth.make_scene(cfg, 0)
+    views = [0, 150]
+    maps = synth.make_region_maps_torch(cfg, torch.device("cuda"), seed=0, views=views).cpu().numpy().view(np.uint32)
+    codes = synth.make_codes(cfg, seed=0, views=views)
+    cams = [scene.cameras[v] for v in views]
+    ora = oracle.uplift(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    ties = assert_parity(res, ora, cfg.K)
+    assert ties < 1e-3 * scene.gaussians.count
