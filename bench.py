@@ -241,6 +241,7 @@ def main():
     st = up.stats()  # one step's counters (reset at each step start)
     contrib_step = sum_over_ranks(st["contributions"])
     tests_step = sum_over_ranks(st["support_tests"])
+    entries_step = sum_over_ranks(st["tile_entries"])
 
     up.set_timing(True)
     barrier()
@@ -328,6 +329,7 @@ def main():
                            maps.numel() * 4 / 1e9, Npad * L * 4 / 1e6)},
             "contributions_per_step": int(contrib_step),
             "support_tests_per_step": int(tests_step),
+            "bin_entries_per_step": int(entries_step),
             "device_ms_per_step": {k: tm[k] / args.steps for k in ("preprocess_ms", "binning_ms", "raster_ms", "topk_ms")},
             "roofline": {"bound": "alu", "kernel": "raster_aggregate_kernel", "achieved": achieved,
                          "peak": alu_peak, "unit": "T lane-ops/s", "frac": achieved / alu_peak,

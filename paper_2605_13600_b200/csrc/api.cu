@@ -161,7 +161,7 @@ void ctx_free(Ctx& c) {
     c.evs.clear();
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect,
-                    b.rec0, b.rec1, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp, c.ids_stage};
+                    b.rec0, b.rec1, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, b.bin_count, c.cub_tmp, c.ids_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c.h_total) cudaFreeHost(c.h_total);
@@ -256,12 +256,35 @@ Ctx::EvSet* ev_begin(scoup_uplift* h, Ctx& c) {
 Ctx::EvSet* ev_cur(Ctx& c) { return c.ev_cur >= 0 ? &c.evs[c.ev_cur] : nullptr; }
 
 // Stage 1 of one view: preprocess, depth sort, scan -> total entries (async to pinned host).
-void stage1(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int tiles_y) {
+// Bin size: the smallest power-of-two group of tiles (>= 64x64 px) whose bin count fits one
+// 8-bit radix pass (<= 256 bins); very large images fall back to <= 1024 bins (2 passes).
+Binning choose_binning(int Wd, int Hd) {
+    Binning b;
+    b.tiles_x = (Wd + TILE - 1) / TILE;
+    b.tiles_y = (Hd + TILE - 1) / TILE;
+    const int cand[][2] = {{6, 6}, {7, 6}, {7, 7}, {8, 7}, {8, 8}, {9, 8}, {9, 9}, {10, 9}, {10, 10}, {11, 10},
+                           {11, 11}, {12, 11}, {12, 12}};
+    for (int lim : {256, 1024}) {
+        for (auto& c : cand) {
+            int bx = (Wd + (1 << c[0]) - 1) >> c[0], by = (Hd + (1 << c[1]) - 1) >> c[1];
+            if (bx * by <= lim) {
+                b.bshx = c[0]; b.bshy = c[1]; b.bins_x = bx; b.bins_y = by;
+                return b;
+            }
+        }
+    }
+    b.bshx = b.bshy = 12;
+    b.bins_x = (Wd + 4095) >> 12;
+    b.bins_y = (Hd + 4095) >> 12;
+    return b;
+}
+
+void stage1(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& bn) {
     const int64_t G = h->G;
     ViewBuffers& b = c.vb;
     Ctx::EvSet* es = ev_begin(h, c);
     if (es) CK(cudaEventRecord(es->e[0], c.s));
-    launch_preprocess(h->pg, G, cam, tiles_x, tiles_y, b, h->d_stats + 3, c.s);
+    launch_preprocess(h->pg, G, cam, bn, b, h->d_stats + 3, c.s);
     size_t need = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, (int)G, 0, 32, c.s));
     size_t need2 = 0;
@@ -278,15 +301,23 @@ void stage1(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int tiles_y
 }
 
 // Stage 2: emit, tile sort, ranges, raster.  Requires stage 1's total on the host.
-scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int tiles_y, const uint32_t* ids,
+scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& bn, const uint32_t* ids,
                     int64_t code_row0, int32_t num_regions, int S, long long* contrib_out, long long pixel_base) {
     CK(cudaEventSynchronize(c.ev_total));
     const uint64_t E = *c.h_total;
-    const int ntiles = tiles_x * tiles_y;
+    const int nbins = bn.nbins();
     ViewBuffers& b = c.vb;
     if (E >= (uint64_t)INT32_MAX)
         return fail(SCOUP_EUNSUPPORTED, "view produces " + std::to_string(E) + " tile entries (>= 2^31)");
-    grow(&b.ranges, &c.t_cap, (size_t)ntiles, 1.0);
+    if ((size_t)nbins > c.t_cap || !b.ranges) {
+        if (b.ranges) CK(cudaFree(b.ranges));
+        if (b.bin_count) CK(cudaFree(b.bin_count));
+        b.ranges = nullptr;
+        b.bin_count = nullptr;
+        CK(cudaMalloc((void**)&b.ranges, sizeof(uint2) * nbins));
+        CK(cudaMalloc((void**)&b.bin_count, sizeof(uint32_t) * nbins));
+        c.t_cap = nbins;
+    }
     h->host_entries += (int64_t)E;
     Ctx::EvSet* es = ev_cur(c);
     if (es) CK(cudaEventRecord(es->e[2], c.s));
@@ -305,18 +336,17 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, int tiles_x, int
             (void)cap;
             c.e_cap = n;
         }
-        launch_emit(b.gidx_sorted, b.offsets, b.rect, tiles_x, h->G, b.ekey, b.eval, c.s);
-        const int nbits = bits_for((uint32_t)ntiles);
+        CK(cudaMemsetAsync(b.bin_count, 0, sizeof(uint32_t) * nbins, c.s));
+        launch_emit(b.gidx_sorted, b.offsets, b.rect, bn, h->G, b.ekey, b.eval, b.bin_count, c.s);
+        launch_ranges_from_counts(b.bin_count, nbins, b.ranges, c.s);
+        const int nbits = bits_for((uint32_t)nbins);
         size_t need = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
         ctx_reserve_cub(c, need);
         CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
-        CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * ntiles, c.s));
-        launch_ranges(b.ekey_alt, (int64_t)E, b.ranges, c.s);
         RasterParams p{};
         p.cam = cam;
-        p.tiles_x = tiles_x;
-        p.tiles_y = tiles_y;
+        p.bn = bn;
         p.ranges = b.ranges;
         p.eval = b.eval_alt;
         p.rec0 = b.rec0;
@@ -480,7 +510,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
     }
     if ((int64_t)Wd * Hd >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "image too large");
     if (h->G == 0) return SCOUP_OK;
-    const int tiles_x = (Wd + TILE - 1) / TILE, tiles_y = (Hd + TILE - 1) / TILE;
+    const Binning bn = choose_binning(Wd, Hd);
     const int64_t npx = (int64_t)Wd * Hd;
     try {
         DeviceGuard dg(h->device);
@@ -533,12 +563,12 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
                 Ctx& c = h->ctx[v & 1];
                 c.view = v;
                 c.ids_dev = ids_for(c, v);
-                stage1(h, c, cams[v], tiles_x, tiles_y);
+                stage1(h, c, cams[v], bn);
             }
             if (v > 0) {
                 Ctx& c = h->ctx[(v - 1) & 1];
                 const int u = v - 1;
-                st = stage2(h, c, cams[u], tiles_x, tiles_y, c.ids_dev, code_row0[u], num_regions[u], S,
+                st = stage2(h, c, cams[u], bn, c.ids_dev, code_row0[u], num_regions[u], S,
                             contributions_out ? (long long*)contributions_out + u : nullptr, (long long)u * npx);
             }
         }

@@ -26,6 +26,15 @@ constexpr int MAX_S = 16;
 #define K_HALF_LOG2E (-0x1.715476p-1f)
 #define K_LOG2E_NEG (-0x1.715476p+0f)
 
+// Pixel tiling: 16x16 raster tiles, grouped into power-of-two bins (multiples of a tile) whose
+// depth-ordered Gaussian lists are what the binning sort produces.
+struct Binning {
+    int tiles_x, tiles_y;   // raster tiles
+    int bshx, bshy;         // log2 of the bin size in pixels (>= 4)
+    int bins_x, bins_y;     // bins
+    int nbins() const { return bins_x * bins_y; }
+};
+
 struct Camera {
     float fx, fy, cx, cy;
     int width, height;
@@ -48,14 +57,15 @@ struct ViewBuffers {
     uint32_t* gidx_sorted;   // [G] Gaussian ids in (depth, index) order
     uint32_t* tiles;         // [G] tile count
     uint64_t* offsets;       // [G] inclusive scan of tiles in depth order
-    uint2* rect;             // [G] (tx0 | ty0<<16, tx1 | ty1<<16)
+    uint2* rect;             // [G] bin rect (bx0 | by0<<16, bx1 | by1<<16), exclusive ends
     float4* rec0;            // [G]
     float4* rec1;            // [G]
     uint32_t* ekey;          // [E] tile id of each (Gaussian, tile) entry
     uint32_t* eval;          // [E] Gaussian id
     uint32_t* ekey_alt;      // [E] sort scratch
     uint32_t* eval_alt;      // [E]
-    uint2* ranges;           // [tiles] [begin, end) into the sorted entries
+    uint2* ranges;           // [bins] [begin, end) into the sorted entries
+    uint32_t* bin_count;     // [bins] entries per bin (histogram of emission)
 };
 
 struct ErrorLatch {
@@ -72,19 +82,19 @@ __device__ __forceinline__ void latch_error(ErrorLatch e, int kind, long long id
 // ---- launchers (kernels.cu) ----
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);
-void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, int tiles_x, int tiles_y,
-                       ViewBuffers vb, unsigned long long* visible_ctr, cudaStream_t s);
+void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, Binning bn, ViewBuffers vb,
+                       unsigned long long* visible_ctr, cudaStream_t s);
 void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles, uint64_t* out,
                               int64_t G, cudaStream_t s);
-void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, int tiles_x,
-                 int64_t G, uint32_t* ekey, uint32_t* eval, cudaStream_t s);
-void launch_ranges(const uint32_t* keys, int64_t E, uint2* ranges, cudaStream_t s);
+void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, Binning bn,
+                 int64_t G, uint32_t* ekey, uint32_t* eval, uint32_t* bin_count, cudaStream_t s);
+void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s);
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K,
                          int L, uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s);
 
 struct RasterParams {
     Camera cam;
-    int tiles_x, tiles_y;
+    Binning bn;
     const uint2* ranges;
     const uint32_t* eval;
     const float4* rec0;

@@ -74,9 +74,8 @@ __global__ void activate_kernel(const float* __restrict__ means, const float* __
 }
 
 // ------------------------------------------------------------------ preprocess (V1-V7)
-__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, Camera cam,
-                                                         int tiles_x, int tiles_y, ViewBuffers vb,
-                                                         unsigned long long* visible_ctr) {
+__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, Camera cam, Binning bn,
+                                                         ViewBuffers vb, unsigned long long* visible_ctr) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool vis = false;
     if (i < G) {
@@ -157,7 +156,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                 if (finite && fx1 >= 0.f && fx0 <= Wm1 && fy1 >= 0.f && fy0 <= Hm1) {
                     int x0 = (int)fmaxf(fx0, 0.f), x1 = (int)fminf(fx1, Wm1);
                     int y0 = (int)fmaxf(fy0, 0.f), y1 = (int)fminf(fy1, Hm1);
-                    int tx0 = x0 / TILE, tx1 = x1 / TILE + 1, ty0 = y0 / TILE, ty1 = y1 / TILE + 1;
+                    int tx0 = x0 >> bn.bshx, tx1 = (x1 >> bn.bshx) + 1, ty0 = y0 >> bn.bshy, ty1 = (y1 >> bn.bshy) + 1;
                     ntiles = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
                     key = __float_as_uint(t[2]);
                     vb.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
@@ -183,22 +182,18 @@ __global__ void gather_tiles_kernel(const uint32_t* __restrict__ gidx_sorted, co
 
 // ------------------------------------------------------------------ emit
 // Entry m of the Gaussian at depth position k goes to slot offsets[k-1] + m, so the
-// entries are in (depth, index) order before the stable tile sort.
-__device__ __forceinline__ void emit_range(uint32_t g, uint2 rect, int tiles_x, uint64_t off, uint32_t m0,
-                                           uint32_t m1, uint32_t* ekey, uint32_t* eval) {
-    uint32_t tx0 = rect.x & 0xFFFFu, ty0 = rect.x >> 16, tx1 = rect.y & 0xFFFFu;
-    uint32_t w = tx1 - tx0;
-    for (uint32_t m = m0; m < m1; m++) {
-        uint32_t ty = ty0 + m / w, tx = tx0 + m % w;
-        ekey[off + m] = ty * (uint32_t)tiles_x + tx;
-        eval[off + m] = g;
-    }
-}
+// entries are in (depth, index) order before the stable bin sort.  Per-bin entry counts are
+// accumulated through a shared-memory histogram (they give the bin ranges directly).
+constexpr int MAX_BINS = 1024;
 
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ gidx_sorted,
                                                    const uint64_t* __restrict__ offsets,
-                                                   const uint2* __restrict__ rect, int tiles_x, int64_t G,
-                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
+                                                   const uint2* __restrict__ rect, int bins_x, int nbins, int64_t G,
+                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
+                                                   uint32_t* __restrict__ bin_count) {
+    __shared__ uint32_t hist[MAX_BINS];
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint64_t begin = 0, end = 0;
@@ -212,32 +207,53 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
             rc = rect[g];
         }
     }
-    uint32_t cnt = (uint32_t)(end - begin);
-    const uint32_t SMALL = 8;
-    if (cnt > 0 && cnt <= SMALL) emit_range(g, rc, tiles_x, begin, 0, cnt, ekey, eval);
-    unsigned big = __ballot_sync(0xffffffffu, cnt > SMALL);
-    while (big) {
-        int src = __ffs(big) - 1;
-        big &= big - 1;
-        uint32_t sg = __shfl_sync(0xffffffffu, g, src);
-        uint32_t rx = __shfl_sync(0xffffffffu, rc.x, src), ry = __shfl_sync(0xffffffffu, rc.y, src);
-        uint64_t sb = __shfl_sync(0xffffffffu, begin, src);
-        uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
-        uint32_t tx0 = rx & 0xFFFFu, ty0 = rx >> 16, w = (ry & 0xFFFFu) - tx0;
-        for (uint32_t m = lane; m < sc; m += 32) {
-            uint32_t ty = ty0 + m / w, tx = tx0 + m % w;
-            ekey[sb + m] = ty * (uint32_t)tiles_x + tx;
-            eval[sb + m] = sg;
+    const uint32_t cnt = (uint32_t)(end - begin);
+    const uint32_t SMALL = 4;
+    if (cnt > 0 && cnt <= SMALL) {
+        const uint32_t bx0 = rc.x & 0xFFFFu, by0 = rc.x >> 16, w = (rc.y & 0xFFFFu) - bx0;
+        for (uint32_t m = 0; m < cnt; m++) {
+            const uint32_t key = (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
+            ekey[begin + m] = key;
+            eval[begin + m] = g;
+            atomicAdd(&hist[key], 1u);
         }
     }
+    unsigned big = __ballot_sync(0xffffffffu, cnt > SMALL);
+    while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const uint32_t sg = __shfl_sync(0xffffffffu, g, src);
+        const uint32_t rx = __shfl_sync(0xffffffffu, rc.x, src), ry = __shfl_sync(0xffffffffu, rc.y, src);
+        const uint64_t sb = __shfl_sync(0xffffffffu, begin, src);
+        const uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
+        const uint32_t bx0 = rx & 0xFFFFu, by0 = rx >> 16, w = (ry & 0xFFFFu) - bx0;
+        for (uint32_t m = lane; m < sc; m += 32) {
+            const uint32_t key = (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
+            ekey[sb + m] = key;
+            eval[sb + m] = sg;
+            atomicAdd(&hist[key], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+        if (hist[i]) atomicAdd(&bin_count[i], hist[i]);
 }
 
-__global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t E, uint2* __restrict__ ranges) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= E) return;
-    uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
-    if (i == E - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+// Exclusive scan of the bin counts -> [begin, end) per bin (one CTA, nbins <= MAX_BINS).
+__global__ void __launch_bounds__(MAX_BINS) ranges_from_counts_kernel(const uint32_t* __restrict__ cnt, int nbins,
+                                                                      uint2* __restrict__ ranges) {
+    __shared__ uint32_t sc[MAX_BINS];
+    const int t = threadIdx.x;
+    uint32_t c = t < nbins ? cnt[t] : 0u;
+    sc[t] = c;
+    __syncthreads();
+    for (int o = 1; o < MAX_BINS; o <<= 1) {
+        uint32_t v = t >= o ? sc[t - o] : 0u;
+        __syncthreads();
+        sc[t] += v;
+        __syncthreads();
+    }
+    if (t < nbins) ranges[t] = make_uint2(sc[t] - c, sc[t]);
 }
 
 // ------------------------------------------------------------------ ingest codes
@@ -384,10 +400,10 @@ void launch_activate(const float* means, const float* scales, const float* rots,
     activate_kernel<<<grid_for(G, 256), 256, 0, s>>>(means, scales, rots, opac, G, pg, err);
 }
 
-void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, int tiles_x, int tiles_y, ViewBuffers vb,
+void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, Binning bn, ViewBuffers vb,
                        unsigned long long* visible_ctr, cudaStream_t s) {
     if (G <= 0) return;
-    preprocess_kernel<<<grid_for(G, 256), 256, 0, s>>>(pg, G, cam, tiles_x, tiles_y, vb, visible_ctr);
+    preprocess_kernel<<<grid_for(G, 256), 256, 0, s>>>(pg, G, cam, bn, vb, visible_ctr);
 }
 
 void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles, uint64_t* out, int64_t G,
@@ -396,15 +412,15 @@ void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles
     gather_tiles_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, tiles, out, G);
 }
 
-void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, int tiles_x, int64_t G,
-                 uint32_t* ekey, uint32_t* eval, cudaStream_t s) {
+void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, Binning bn, int64_t G,
+                 uint32_t* ekey, uint32_t* eval, uint32_t* bin_count, cudaStream_t s) {
     if (G <= 0) return;
-    emit_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, offsets, rect, tiles_x, G, ekey, eval);
+    emit_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, offsets, rect, bn.bins_x, bn.nbins(), G, ekey, eval,
+                                                 bin_count);
 }
 
-void launch_ranges(const uint32_t* keys, int64_t E, uint2* ranges, cudaStream_t s) {
-    if (E <= 0) return;
-    ranges_kernel<<<grid_for(E, 256), 256, 0, s>>>(keys, E, ranges);
+void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s) {
+    ranges_from_counts_kernel<<<1, MAX_BINS, 0, s>>>(bin_count, nbins, ranges);
 }
 
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K, int L,

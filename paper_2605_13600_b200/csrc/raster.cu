@@ -1,20 +1,26 @@
 // raster.cu -- fused rasterise-and-aggregate kernel (the hot loop of Algorithm 1).
 //
-// One CTA of 256 threads per 16x16 tile, one pixel per thread (natural row-major order, so
-// a warp is a 16x2 pixel block).  The tile's Gaussian list (depth order) is walked in
-// batches of 32 records staged in shared memory (double-buffered, prefetched by warp 0).
-// Per pixel and Gaussian the thread applies DESIGN.md §3 step PX -- square support, the
-// log2-domain quadratic form, the y <= 0 guard, alpha = min(0.99, o exp2_spec(y)), the
-// alpha >= 1/255 skip and the T(1-alpha) < 1e-4 stop -- giving e_i(v,p) = alpha_i T
-// (Eq. 2) bit-identical to the CPU oracle.
+// One CTA of 256 threads per 16x16 tile, one pixel per thread (row-major: a warp is a 16x2
+// pixel block).  The tile reads the depth-ordered Gaussian list of the bin that contains it
+// (bins are power-of-two groups of tiles) and walks it front to back:
 //
-// Aggregation (Eq. 5; Algorithm 1 lines 8-10): the 32 per-pixel
-// weights of a batch are summed over the pixels of each (warp, region) group with a
-// 31-shuffle transpose-reduction (lane l ends with the group's sum for Gaussian l), the
-// group sums of all warps are combined per (tile region, Gaussian) in shared memory, and
-// only then do global reductions go out: S `red.global.add.f32` per (tile region,
-// Gaussian) into W[g][atom] (value c * sum e) plus one per Gaussian into Z[g].  A tile with
-// more than MAX_SLOTS distinct regions falls back to per-pixel reductions.
+//  refill   256 candidates at a time are tested against the tile (square support and the
+//           alpha >= 1/255 ellipse, conservatively) and stably compacted into a shared-memory
+//           ring of records, so the ring stays in (depth, index) order;
+//  batch    32 ring records at a time: each warp builds the mask of records whose support
+//           touches its 16x2 block (exact row intervals, conservative margins) and evaluates
+//           only those, in order, per pixel -- DESIGN.md §3 step PX: square test, the
+//           log2-domain quadratic form, the q <= 0 guard, alpha = min(0.99, o exp2_spec(q)),
+//           the alpha >= 1/255 skip and the T(1-alpha) < 1e-4 stop -- giving the weights
+//           e_i(v,p) = alpha_i T of PAPER.md Eq. 2, bit-identical to the CPU oracle.
+//
+// Aggregation (Eq. 5; Algorithm 1 lines 8-10): per warp and region
+// group, the per-pixel weights of the batch are summed with a 31-shuffle transpose-reduction
+// (lane l ends with the sum of the l-th evaluated Gaussian), the group sums of all warps are
+// combined per (tile region, Gaussian) in shared memory, and only then global reductions go
+// out: S `red.global.add.f32` per (tile region, Gaussian) into W[g][atom] (c * sum e) plus one
+// per Gaussian into Z[g].  A tile with more than MAX_SLOTS distinct regions falls back to
+// per-pixel reductions.
 #include "internal.cuh"
 
 namespace scoup {
@@ -22,8 +28,10 @@ namespace scoup {
 namespace {
 
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;   // unassigned or outside the image
-constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // hash-table sentinel (never a region id here)
+constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // hash-table sentinel
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + BATCH)
+constexpr int NWARP = TILE_PIX / 32;
 
 // DESIGN.md §3 exp2_spec for ycut <= y <= 0 (the caller's conservative prune guarantees
 // y >= ycut > -64, so the oracle's y < -64 branch is unreachable here).
@@ -43,7 +51,46 @@ __device__ __forceinline__ float exp2_spec(float y) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Sum e[j] over the lanes of `grp` (all lanes if grp == FULL); lane l returns the sum for j = l.
+// Interval of u (offset along a line) where a u^2 + b u + c >= 0, a < 0.  Empty -> lo > hi.
+__device__ __forceinline__ void quad_interval(float a, float b, float c, float& lo, float& hi) {
+    const float D = b * b - 4.f * a * c;
+    if (D < 0.f) { lo = 1.f; hi = -1.f; return; }
+    const float s = sqrtf(D), inv = 0.5f / a;  // inv < 0
+    lo = (s - b) * inv;
+    hi = (-b - s) * inv;
+}
+
+// Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut) produce a
+// fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r
+// (square support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative); the
+// rectangle is widened by 0.5 px and ycut relaxed by 0.01 so fp32 rounding here can only
+// accept more.  Exact per-pixel decisions are made in the evaluation.
+__device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float X0, float X1, float Y0, float Y1) {
+    const float M = 0.5f;
+    X0 -= M; X1 += M; Y0 -= M; Y1 += M;
+    const float mx = a.x, my = a.y, r = a.z;
+    if (r < 0.f) return false;
+    // square support
+    if (mx + r < X0 || mx - r > X1 || my + r < Y0 || my - r > Y1) return false;
+    // ellipse {q >= yc}: centre inside, or it crosses an edge of the rectangle
+    if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
+    const float qa = b.x, qb = b.y, qc = b.z, yc = b.w - 0.01f;
+    float lo, hi;
+    const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
+    // horizontal edges (dy fixed): qa dx^2 + qb dy dx + (qc dy^2 - yc) >= 0
+    quad_interval(qa, qb * ey0, qc * ey0 * ey0 - yc, lo, hi);
+    if (lo <= hi && hi >= ex0 && lo <= ex1) return true;
+    quad_interval(qa, qb * ey1, qc * ey1 * ey1 - yc, lo, hi);
+    if (lo <= hi && hi >= ex0 && lo <= ex1) return true;
+    // vertical edges (dx fixed): qc dy^2 + qb dx dy + (qa dx^2 - yc) >= 0
+    quad_interval(qc, qb * ex0, qa * ex0 * ex0 - yc, lo, hi);
+    if (lo <= hi && hi >= ey0 && lo <= ey1) return true;
+    quad_interval(qc, qb * ex1, qa * ex1 * ex1 - yc, lo, hi);
+    if (lo <= hi && hi >= ey0 && lo <= ey1) return true;
+    return false;
+}
+
+// Sum e[i] over the lanes in the group (all lanes if !MASKED); lane l returns the sum for i = l.
 template <bool MASKED>
 __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool mine, int lane) {
     float v[16];
@@ -53,8 +100,8 @@ __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool 
         for (int i = 0; i < 16; i++) {
             float lo = e[i], hi = e[i + 16];
             if (MASKED) { lo = mine ? lo : 0.f; hi = mine ? hi : 0.f; }
-            float send = up ? lo : hi;
-            float keep = up ? hi : lo;
+            const float send = up ? lo : hi;
+            const float keep = up ? hi : lo;
             v[i] = keep + __shfl_xor_sync(FULL, send, 16);
         }
     }
@@ -63,41 +110,58 @@ __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool 
         const bool up = lane & s;
 #pragma unroll
         for (int i = 0; i < s; i++) {
-            float send = up ? v[i] : v[i + s];
-            float keep = up ? v[i + s] : v[i];
+            const float send = up ? v[i] : v[i + s];
+            const float keep = up ? v[i + s] : v[i];
             v[i] = keep + __shfl_xor_sync(FULL, send, s);
         }
     }
     return v[0];
 }
 
+// Fallback aggregation of one fragment (code_row < 0: unassigned pixel, Z only).
+__device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* atoms, const float* coefs, int S,
+                                           int L, uint32_t g, float ev, int64_t code_row) {
+    atomicAdd(Z + g, ev);
+    if (code_row < 0) return;
+    for (int s = 0; s < S; s++) {
+        const uint32_t at = __ldg(atoms + code_row + s);
+        if (at != NONE) atomicAdd(W + (int64_t)g * L + at, __fmul_rn(__ldg(coefs + code_row + s), ev));
+    }
+}
+
 struct __align__(16) Smem {
-    float4 rec0[2][BATCH];
-    float4 rec1[2][BATCH];
-    uint32_t gid[2][BATCH];
+    float4 q0[QCAP];   // ring of candidate records: (mx, my, r, o)
+    float4 q1[QCAP];   //                            (qa, qb, qc, ycut)
+    uint32_t qg[QCAP]; //                            Gaussian id
     float acc[2][MAX_SLOTS * BATCH];
     float accZ[2][BATCH];
     uint32_t slot_key[MAX_SLOTS];
     uint32_t slot_atom[MAX_SLOTS][MAX_S];
     float slot_coef[MAX_SLOTS][MAX_S];
+    int wcnt[NWARP];
     int nslot;
     int overflow;
     unsigned long long contrib;
     unsigned long long tests;
 };
 
-__device__ __forceinline__ void smem_add(float* p, float v) { atomicAdd(p, v); }
-
 __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const RasterParams p) {
-    __shared__ Smem sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int tile = blockIdx.x;
-    const uint2 range = p.ranges[tile];
+    const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
+    const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
+    const uint2 range = p.ranges[bin];
     if (range.x >= range.y) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x = tx * TILE + (t & (TILE - 1)), y = ty * TILE + (t >> 4);
     const int Wd = p.cam.width, Hd = p.cam.height;
     const bool inside = x < Wd && y < Hd;
+    // pixel-centre rectangles of the tile and of this warp's 16x2 block (clipped to the image)
+    const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
+    const float TX1 = (float)(min(tx * TILE + TILE, Wd) - 1) + 0.5f;
+    const float TY1 = (float)(min(ty * TILE + TILE, Hd) - 1) + 0.5f;
+    const float WY0 = (float)(ty * TILE + 2 * warp) + 0.5f, WY1 = WY0 + 1.f;
 
     // ---- setup: region key of my pixel, tile slot table, slot codes
     uint32_t key = KEY_NONE;
@@ -113,27 +177,13 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
     if (t == 0) { sm.nslot = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; }
     for (int i = t; i < 2 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
     if (t < 2 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
-    // first batch of records (warp 0)
-    const uint32_t nent = range.y - range.x;
-    if (warp == 0) {
-        uint32_t g = 0;
-        float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if ((uint32_t)lane < nent) {
-            g = __ldg(p.eval + range.x + lane);
-            r0 = __ldg(p.rec0 + g);
-            r1 = __ldg(p.rec1 + g);
-        }
-        sm.gid[0][lane] = g;
-        sm.rec0[0][lane] = r0;
-        sm.rec1[0][lane] = r1;
-    }
     __syncthreads();
     const unsigned grp = __match_any_sync(FULL, key);
     const int leader = __ffs(grp) - 1;
     int slot = -1;
     if (lane == leader) {
         for (int q = 0; q < MAX_SLOTS; q++) {
-            uint32_t old = atomicCAS(&sm.slot_key[q], SLOT_EMPTY, key);
+            const uint32_t old = atomicCAS(&sm.slot_key[q], SLOT_EMPTY, key);
             if (old == SLOT_EMPTY || old == key) { slot = q; break; }
         }
         if (slot < 0) sm.overflow = 1;
@@ -157,7 +207,9 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
         sm.slot_atom[q][s] = a;
         sm.slot_coef[q][s] = c;
     }
-    // no barrier needed yet: slot codes are first read after the first B1 barrier
+    // (slot codes are first read after a later barrier)
+    const bool coded = key != KEY_NONE;
+    const int64_t my_code_row = (p.code_row0 + (int64_t)(coded ? key : 0)) * S;
 
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
     float T = 1.0f;
@@ -165,32 +217,74 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
     uint32_t cnt = 0, tests = 0;
     float* Wm = p.W;
     const int L = p.L;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
 
+    uint32_t cursor = range.x;
+    uint32_t q_head = 0, q_count = 0;
     int buf = 0;
-    for (uint32_t base = range.x; base < range.y; base += BATCH, buf ^= 1) {
-        const uint32_t n = min((uint32_t)BATCH, range.y - base);
-        // prefetch next batch's records into registers (warp 0)
-        uint32_t ng = 0;
-        float4 nr0 = make_float4(0.f, 0.f, -1.f, 0.f), nr1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        const uint32_t nbase = base + BATCH;
-        if (warp == 0 && nbase + lane < range.y) {
-            ng = __ldg(p.eval + nbase + lane);
-            nr0 = __ldg(p.rec0 + ng);
-            nr1 = __ldg(p.rec1 + ng);
-        }
-
-        // ---- rasterise: e[j] for the batch (DESIGN.md §3 step PX)
-        float e[BATCH];
-        bool any = false;
+    while (true) {
+        // ---- refill the ring with candidates relevant to this tile (stable compaction)
+        while (q_count < (uint32_t)BATCH && cursor < range.y) {
+            const uint32_t idx = cursor + t;
+            bool acc = false;
+            uint32_t g = 0;
+            float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (idx < range.y) {
+                g = __ldg(p.eval + idx);
+                r0 = __ldg(p.rec0 + g);
+                r1 = __ldg(p.rec1 + g);
+                acc = rect_relevant(r0, r1, TX0, TX1, TY0, TY1);
+            }
+            const unsigned bal = __ballot_sync(FULL, acc);
+            if (lane == 0) sm.wcnt[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t off = 0, tot = 0;
 #pragma unroll
-        for (int j = 0; j < BATCH; j++) {
-            e[j] = 0.f;
+            for (int w = 0; w < NWARP; w++) {
+                const uint32_t c = (uint32_t)sm.wcnt[w];
+                off += (w < warp) ? c : 0u;
+                tot += c;
+            }
+            if (acc) {
+                const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
+                sm.qg[pos] = g;
+                sm.q0[pos] = r0;
+                sm.q1[pos] = r1;
+            }
+            q_count += tot;
+            cursor += TILE_PIX;
+            __syncthreads();
+        }
+        if (q_count == 0) break;
+        const uint32_t n = min((uint32_t)BATCH, q_count);
+
+        // ---- per-warp mask of batch records touching this warp's 16x2 block
+        const bool warp_done = __all_sync(FULL, done);
+        bool rel = false;
+        if (!warp_done && (uint32_t)lane < n) {
+            const uint32_t pos = (q_head + lane) & (QCAP - 1);
+            rel = rect_relevant(sm.q0[pos], sm.q1[pos], TX0, TX1, WY0, WY1);
+        }
+        const unsigned mask = __ballot_sync(FULL, rel);
+
+        // ---- rasterise: e[i] for the i-th relevant record, in depth order (DESIGN.md §3 PX)
+        float e[BATCH];
+#pragma unroll
+        for (int i = 0; i < BATCH; i++) e[i] = 0.f;
+        bool any = false;
+        unsigned m = mask;
+#pragma unroll
+        for (int i = 0; i < BATCH; i++) {
+            if (m == 0u) break;
+            const int j = __ffs(m) - 1;
+            m &= m - 1u;
             if (!done) {
-                const float4 a = sm.rec0[buf][j];  // mx, my, r, o  (r = -1 for padding)
+                const uint32_t pos = (q_head + j) & (QCAP - 1);
+                const float4 a = sm.q0[pos];  // mx, my, r, o
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
                 if (fabsf(dx) <= a.z && fabsf(dy) <= a.z) {
                     tests++;
-                    const float4 b = sm.rec1[buf][j];  // qa, qb, qc, ycut
+                    const float4 b = sm.q1[pos];  // qa, qb, qc, ycut
                     const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
                                               __fmul_rn(__fmul_rn(b.z, dy), dy));
                     if (!(q > 0.f) && q >= b.w) {
@@ -200,7 +294,8 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                             if (Tn < K_TMIN) {
                                 done = true;
                             } else {
-                                e[j] = __fmul_rn(al, T);
+                                const float ev = __fmul_rn(al, T);
+                                e[i] = ev;
                                 T = Tn;
                                 cnt++;
                                 any = true;
@@ -210,16 +305,34 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                 }
             }
         }
+        if (overflow && any) {
+            // per-pixel reductions straight from the code table (tiles with > MAX_SLOTS regions)
+            unsigned m2 = mask;
+#pragma unroll
+            for (int i = 0; i < BATCH; i++) {
+                if (m2 == 0u) break;
+                const int j = __ffs(m2) - 1;
+                m2 &= m2 - 1u;
+                if (e[i] > 0.f)
+                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, sm.qg[(q_head + j) & (QCAP - 1)], e[i],
+                                  coded ? my_code_row : -1);
+            }
+        }
 
         if (!overflow) {
             // ---- per (warp, region group) transpose-reduction, then shared accumulation
             if (__any_sync(FULL, any)) {
-                float zsum = 0.f;
+                const bool mine_rel = (mask >> lane) & 1u;
+                const int rank = __popc(mask & lanemask_lt);
                 if (grp == FULL) {
                     const float v = transpose_reduce<false>(e, true, lane);
-                    if (v != 0.f) smem_add(&sm.acc[buf][slot * BATCH + lane], v);
-                    zsum = v;
+                    const float vj = __shfl_sync(FULL, v, rank & 31);
+                    if (mine_rel && vj != 0.f) {
+                        atomicAdd(&sm.acc[buf][slot * BATCH + lane], vj);
+                        atomicAdd(&sm.accZ[buf][lane], vj);
+                    }
                 } else {
+                    float zsum = 0.f;
                     unsigned todo = FULL;
                     while (todo) {
                         const int l = __ffs(todo) - 1;
@@ -227,11 +340,12 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                         const int q = __shfl_sync(FULL, slot, l);
                         todo &= ~g2;
                         const float v = transpose_reduce<true>(e, (g2 >> lane) & 1u, lane);
-                        if (v != 0.f) smem_add(&sm.acc[buf][q * BATCH + lane], v);
-                        zsum += v;
+                        const float vj = __shfl_sync(FULL, v, rank & 31);
+                        if (mine_rel && vj != 0.f) atomicAdd(&sm.acc[buf][q * BATCH + lane], vj);
+                        zsum += mine_rel ? vj : 0.f;
                     }
+                    if (zsum != 0.f) atomicAdd(&sm.accZ[buf][lane], zsum);
                 }
-                if (zsum != 0.f) smem_add(&sm.accZ[buf][lane], zsum);
             }
             __syncthreads();  // B1
             // ---- flush: S reds per (slot, Gaussian) into W, one per Gaussian into Z
@@ -243,49 +357,26 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                 const float v = sm.acc[buf][q * BATCH + j];
                 const uint32_t a = sm.slot_atom[q][s];
                 if (v > 0.f && a != NONE)
-                    atomicAdd(Wm + (int64_t)sm.gid[buf][j] * L + a, __fmul_rn(sm.slot_coef[q][s], v));
+                    atomicAdd(Wm + (int64_t)sm.qg[(q_head + j) & (QCAP - 1)] * L + a,
+                              __fmul_rn(sm.slot_coef[q][s], v));
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
-                if (z > 0.f) atomicAdd(p.Z + sm.gid[buf][t], z);
+                if (z > 0.f) atomicAdd(p.Z + sm.qg[(q_head + t) & (QCAP - 1)], z);
             }
-            // zero the other accumulator buffer (last flushed one batch ago)
+            // zero the other accumulator buffer (flushed one batch ago)
             for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[buf ^ 1][i] = 0.f;
             if (t < BATCH) sm.accZ[buf ^ 1][t] = 0.f;
-        } else {
-            // ---- fallback: per-pixel reductions straight from the code table
-            if (any) {
-                const bool coded = key != KEY_NONE;
-                const int64_t row = (p.code_row0 + (int64_t)(coded ? key : 0)) * S;
-#pragma unroll 1
-                for (int j = 0; j < BATCH; j++) {
-                    if (e[j] > 0.f) {
-                        const uint32_t g = sm.gid[buf][j];
-                        atomicAdd(p.Z + g, e[j]);
-                        if (coded) {
-                            for (int s = 0; s < S; s++) {
-                                const uint32_t a = __ldg(p.code_atoms + row + s);
-                                if (a != NONE)
-                                    atomicAdd(Wm + (int64_t)g * L + a, __fmul_rn(__ldg(p.code_coefs + row + s), e[j]));
-                            }
-                        }
-                    }
-                }
-            }
         }
-        // stage the prefetched records for the next batch
-        if (warp == 0) {
-            sm.gid[buf ^ 1][lane] = ng;
-            sm.rec0[buf ^ 1][lane] = nr0;
-            sm.rec1[buf ^ 1][lane] = nr1;
-        }
+        q_head += n;
+        q_count -= n;
+        buf ^= 1;
         if (__syncthreads_count(!done) == 0) break;  // B2
-        (void)n;
     }
 
-    // contributions (terms of Eq. 5's sum)
-    unsigned c = __reduce_add_sync(FULL, cnt);
-    unsigned ts = __reduce_add_sync(FULL, tests);
+    // contributions (terms of Eq. 5's sum) and support tests
+    const unsigned c = __reduce_add_sync(FULL, cnt);
+    const unsigned ts = __reduce_add_sync(FULL, tests);
     if (lane == 0 && c) atomicAdd(&sm.contrib, (unsigned long long)c);
     if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
     __syncthreads();
@@ -301,9 +392,10 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
 }  // namespace
 
 void launch_raster(const RasterParams& p, cudaStream_t s) {
-    const int ntiles = p.tiles_x * p.tiles_y;
+    const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
     if (ntiles <= 0) return;
-    raster_aggregate_kernel<<<ntiles, TILE_PIX, 0, s>>>(p);
+    static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the default 48 KB window");
+    raster_aggregate_kernel<<<ntiles, TILE_PIX, sizeof(Smem), s>>>(p);
 }
 
 }  // namespace scoup

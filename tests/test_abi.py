@@ -77,7 +77,7 @@ def test_sass_uses_global_reductions(lib):
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", abi.LIB_PATH], capture_output=True,
                           text=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
-    raster = [f for f in funcs if f.split("\n", 1)[0].find("raster_aggregate_kernel") >= 0]
+    raster = "".join(f for f in funcs if f.split("\n", 1)[0].find("raster_cu") >= 0)
     assert raster, "raster kernel not found in SASS"
-    assert "REDG.E.ADD.F32" in raster[0]
-    assert "ATOMG.E.ADD.F32" not in raster[0]
+    assert "REDG.E.ADD.F32" in raster
+    assert "ATOMG.E.ADD.F32" not in raster
