@@ -137,14 +137,25 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                 // an ill-conditioned det cannot shrink it) and padded; exact test per pixel.
                 float hx = r, hy = r;
                 {
+                    // The pixel's fp32 q has absolute error ~ eps * (size of its terms), which for
+                    // far off-screen near-plane Gaussians is not negligible: widen the level set by
+                    // 1e-6 * (bound on the terms over the current box), twice.
                     double dca = ca, dcb = cb, dcc = cc;
                     double detc = dca * dcc - dcb * dcb;
-                    double m2 = -2.0 * 0.6931471805599453 * (double)ycut;
-                    if (detc > 0.0 && m2 > 0.0) {
-                        double ex = sqrt(m2 * dcc / detc) * 1.001 + 0.01;
-                        double ey = sqrt(m2 * dca / detc) * 1.001 + 0.01;
-                        hx = (float)fmin((double)r, ex);
-                        hy = (float)fmin((double)r, ey);
+                    if (detc > 0.0) {
+                        double yc = (double)ycut;
+                        double ex = r, ey = r;
+                        for (int it = 0; it < 3; it++) {
+                            double m2 = -2.0 * 0.6931471805599453 * yc;
+                            if (m2 <= 0.0) break;
+                            ex = fmin((double)r, sqrt(m2 * dcc / detc) * 1.001 + 0.01);
+                            ey = fmin((double)r, sqrt(m2 * dca / detc) * 1.001 + 0.01);
+                            double mq = (fabs((double)qa) + 0.5 * fabs((double)qb)) * ex * ex +
+                                        (fabs((double)qc) + 0.5 * fabs((double)qb)) * ey * ey;
+                            yc = (double)ycut - 0.01 - 2e-6 * mq;
+                        }
+                        hx = (float)ex;
+                        hy = (float)ey;
                     }
                 }
                 float padx = 1.0f + 1e-6f * (fabsf(mx) + hx);

@@ -51,20 +51,14 @@ __device__ __forceinline__ float exp2_spec(float y) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Interval of u (offset along a line) where a u^2 + b u + c >= 0, a < 0.  Empty -> lo > hi.
-__device__ __forceinline__ void quad_interval(float a, float b, float c, float& lo, float& hi) {
-    const float D = b * b - 4.f * a * c;
-    if (D < 0.f) { lo = 1.f; hi = -1.f; return; }
-    const float s = sqrtf(D), inv = 0.5f / a;  // inv < 0
-    lo = (s - b) * inv;
-    hi = (-b - s) * inv;
-}
-
 // Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut) produce a
-// fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r
-// (square support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative); the
-// rectangle is widened by 0.5 px and ycut relaxed by 0.01 so fp32 rounding here can only
-// accept more.  Exact per-pixel decisions are made in the evaluation.
+// fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r (square
+// support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative).  Margins make every
+// rounding here (and in the pixel's own fp32 evaluation of q, whose absolute error grows with
+// the size of the quadratic terms, e.g. for far off-screen near-plane Gaussians) only accept
+// more: the rectangle is widened by 0.5 px and ycut relaxed by 0.01 + 2e-6 * (bound on the
+// terms of q over the rectangle).  Chords use the Schur form (peak of q along a line,
+// 4 qa qc - qb^2 in fp64) so elongated ellipses do not lose precision.
 __device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float X0, float X1, float Y0, float Y1) {
     const float M = 0.5f;
     X0 -= M; X1 += M; Y0 -= M; Y1 += M;
@@ -72,21 +66,35 @@ __device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float X0, floa
     if (r < 0.f) return false;
     // square support
     if (mx + r < X0 || mx - r > X1 || my + r < Y0 || my - r > Y1) return false;
-    // ellipse {q >= yc}: centre inside, or it crosses an edge of the rectangle
+    // ellipse {q >= yc}: centre inside, or it meets an edge of the rectangle
     if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
-    const float qa = b.x, qb = b.y, qc = b.z, yc = b.w - 0.01f;
-    float lo, hi;
+    const float qa = b.x, qb = b.y, qc = b.z;
     const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
-    // horizontal edges (dy fixed): qa dx^2 + qb dy dx + (qc dy^2 - yc) >= 0
-    quad_interval(qa, qb * ey0, qc * ey0 * ey0 - yc, lo, hi);
-    if (lo <= hi && hi >= ex0 && lo <= ex1) return true;
-    quad_interval(qa, qb * ey1, qc * ey1 * ey1 - yc, lo, hi);
-    if (lo <= hi && hi >= ex0 && lo <= ex1) return true;
-    // vertical edges (dx fixed): qc dy^2 + qb dx dy + (qa dx^2 - yc) >= 0
-    quad_interval(qc, qb * ex0, qa * ex0 * ex0 - yc, lo, hi);
-    if (lo <= hi && hi >= ey0 && lo <= ey1) return true;
-    quad_interval(qc, qb * ex1, qa * ex1 * ex1 - yc, lo, hi);
-    if (lo <= hi && hi >= ey0 && lo <= ey1) return true;
+    const float dxm = fminf(fmaxf(fabsf(ex0), fabsf(ex1)), r), dym = fminf(fmaxf(fabsf(ey0), fabsf(ey1)), r);
+    const float mq = (fabsf(qa) + 0.5f * fabsf(qb)) * dxm * dxm + (fabsf(qc) + 0.5f * fabsf(qb)) * dym * dym;
+    const float yc = b.w - 0.01f - 2e-6f * mq;
+    const float dq = (float)(4.0 * (double)qa * (double)qc - (double)qb * (double)qb);
+    if (!(dq > 0.f)) return true;  // degenerate form: accept
+    const float ky = dq / (4.f * qa), kx = dq / (4.f * qc);  // peak of q along a row / column, per d^2
+    // rows y = const: q(dx) = qa (dx - c)^2 + ky dy^2 with c = -qb dy / (2 qa)
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const float ey = k ? ey1 : ey0;
+        const float h2 = (ky * ey * ey - yc) / -qa;
+        if (h2 >= 0.f) {
+            const float c = -qb * ey / (2.f * qa), h = sqrtf(h2);
+            if (c + h >= ex0 && c - h <= ex1) return true;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const float ex = k ? ex1 : ex0;
+        const float h2 = (kx * ex * ex - yc) / -qc;
+        if (h2 >= 0.f) {
+            const float c = -qb * ex / (2.f * qc), h = sqrtf(h2);
+            if (c + h >= ey0 && c - h <= ey1) return true;
+        }
+    }
     return false;
 }
 

@@ -91,3 +91,34 @@ def compare_codes(atoms_gpu, coefs_gpu, W_ora, K, rtol=1e-4, atol=1e-6):
             if not worst:
                 worst = f"row {i}: gpu {list(zip(sel, coefs_gpu[i][:len(sel)]))} vs oracle top {[(a, w[a]) for a in top]}"
     return bad, ties, worst
+
+
+def extreme_scene(seed=21):
+    """Near-plane off-screen giants, needles, sub-pixel Gaussians, opacity 1/255 and 1.0."""
+    rng = np.random.default_rng(seed)
+    means, scales, rots, opac = [], [], [], []
+    for k in range(40):  # near-plane giants, mostly off-screen
+        z = 0.2 + rng.uniform(1e-4, 0.05)
+        means.append([rng.uniform(-3, 3) * z * 8, rng.uniform(-3, 3) * z * 8, z])
+        scales.append(np.exp(rng.uniform(np.log(0.01), np.log(2.0), 3)))
+        rots.append(rng.normal(size=4))
+        opac.append(rng.uniform(0.01, 1.0))
+    for k in range(200):  # needles
+        means.append(rng.uniform(-1, 1, 3) * [1, 1, 0.5] + [0, 0, 3])
+        s = np.array([1e-3, 1e-3, 1e-3])
+        s[rng.integers(0, 3)] = rng.uniform(0.3, 2.0)
+        scales.append(s)
+        rots.append(rng.normal(size=4))
+        opac.append(rng.uniform(0.05, 1.0))
+    for k in range(200):  # sub-pixel and generic
+        means.append(rng.uniform(-1.5, 1.5, 3) + [0, 0, 4])
+        scales.append(np.exp(rng.normal(np.log(0.002 if k % 2 else 0.05), 0.5, 3)))
+        rots.append(rng.normal(size=4))
+        opac.append([1 / 255, 1.0, 0.5][k % 3])
+    g = gaussians(means, scales, rots, opac)
+    cams = [identity_camera(160, 120, 150.0), synth.look_at_camera(np.array([0.5, -0.3, -1.0]), 160, 120, 75.0)]
+    R = 9
+    yy, xx = np.mgrid[0:120, 0:160]
+    maps = np.stack([((xx // 40) + 4 * (yy // 40)) % R, ((xx // 23) * 7 + (yy // 17)) % R]).astype(np.uint32)
+    codes = synth.make_codes(synth.CONFIGS["tiny"].with_(num_views=2, regions=(R,)), seed=9)
+    return g, cams, maps, codes

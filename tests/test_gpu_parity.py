@@ -254,3 +254,15 @@ def test_outdoor_full_size_sampled_views(dev):
     res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
     ties = assert_parity(res, ora, cfg.K)
     assert ties < 1e-3 * scene.gaussians.count
+
+
+def test_extreme_gaussians(dev):
+    """Degenerate footprints: near-plane off-screen giants (huge conics, strong fp32 cancellation
+    in q), needle-thin rotated Gaussians, sub-pixel Gaussians, opacity at 1/255 and 1.0 -- the
+    conservative tile/warp filters must not drop a single fragment (exact counts)."""
+    from helpers import extreme_scene
+    g, cams, maps, codes = extreme_scene()
+    ora = oracle.uplift(g, cams, maps, codes, 64, 4)
+    assert ora[2].sum() > 1000
+    res = run_gpu(g, cams, maps, codes, 64, 4)
+    assert_parity(res, ora, 4)
