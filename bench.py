@@ -195,15 +195,16 @@ def main():
     scene = synth.make_scene(cfg, 0)
     g = scene.gaussians
     G, L, K = g.count, cfg.L, cfg.K
-    my_views = list(range(rank, cfg.num_views, world))
+    from paper_2605_13600_b200 import distributed as D
+    my_views = D.views_for_rank(cfg.num_views, rank, world)
     cams = [scene.cameras[v] for v in my_views]
     maps = synth.make_region_maps_torch(cfg, dev, seed=0, views=my_views)
     codes_h = synth.make_codes(cfg, seed=0, views=my_views)
     codes = synth.Codes(torch.from_numpy(codes_h.atoms.view(np.int32)).to(dev), torch.from_numpy(codes_h.coefs).to(dev),
                         codes_h.row0, codes_h.num_regions)
     gd = synth.Gaussians(*[torch.from_numpy(a).to(dev) for a in (g.means, g.scales, g.rotations, g.opacities)])
-    Npad = int(math.ceil(G / world) * world)
-    shard = Npad // world
+    Npad = D.padded_rows(G, world)
+    first_row, shard = D.row_shard(G, rank, world)
     up = SparseUplift(gd, L, K, device=local, rows_padded=Npad)
     Ws = torch.empty((shard, L), dtype=torch.float32, device=dev) if world > 1 else None
     Zs = torch.empty((shard,), dtype=torch.float32, device=dev) if world > 1 else None
@@ -212,9 +213,8 @@ def main():
         up.reset()
         up.add_views(cams, maps, codes)
         if world > 1:
-            dist.reduce_scatter_tensor(Ws, up.W)
-            dist.reduce_scatter_tensor(Zs, up.Z)
-            return up.finalize(first_row=rank * shard, num_rows=shard, W_rows=Ws, Z_rows=Zs)
+            D.reduce_scatter_accumulators(up.W, up.Z, Ws, Zs)
+            return up.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs)
         return up.finalize()
 
     def barrier():
@@ -288,9 +288,8 @@ def main():
             u2 = SparseUplift(g_h, L, K, device=local, rows_padded=Npad)
             u2.add_views(cams, maps_h, codes_hp)
             if world > 1:
-                dist.reduce_scatter_tensor(Ws, u2.W)
-                dist.reduce_scatter_tensor(Zs, u2.Z)
-                u2.finalize(first_row=rank * shard, num_rows=shard, W_rows=Ws, Z_rows=Zs,
+                D.reduce_scatter_accumulators(u2.W, u2.Z, Ws, Zs)
+                u2.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs,
                             out_atoms=atoms_h[:shard], out_coefs=coefs_h[:shard])
             else:
                 u2.finalize(0, G, out_atoms=atoms_h[:G], out_coefs=coefs_h[:G])
