@@ -242,6 +242,7 @@ def main():
     contrib_step = sum_over_ranks(st["contributions"])
     tests_step = sum_over_ranks(st["support_tests"])
     entries_step = sum_over_ranks(st["tile_entries"])
+    visible_step = sum_over_ranks(st["visible"])
 
     up.set_timing(True)
     barrier()
@@ -329,6 +330,7 @@ def main():
             "contributions_per_step": int(contrib_step),
             "support_tests_per_step": int(tests_step),
             "bin_entries_per_step": int(entries_step),
+            "visible_per_step": int(visible_step),
             "device_ms_per_step": {k: tm[k] / args.steps for k in ("preprocess_ms", "binning_ms", "raster_ms", "topk_ms")},
             "roofline": {"bound": "alu", "kernel": "raster_aggregate_kernel", "achieved": achieved,
                          "peak": alu_peak, "unit": "T lane-ops/s", "frac": achieved / alu_peak,

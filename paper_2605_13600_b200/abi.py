@@ -13,7 +13,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libscoup.so")
+# SCOUP_LIB: an alternative in-tree build of the same library (A/B kernel variants)
+LIB_PATH = os.environ.get("SCOUP_LIB") or os.path.join(HERE, "libscoup.so")
 
 SCOUP_NONE = 0xFFFFFFFF
 STATUS = {0: "SCOUP_OK", 1: "SCOUP_EINVAL", 2: "SCOUP_EDATA", 3: "SCOUP_ECUDA", 4: "SCOUP_ENOMEM",

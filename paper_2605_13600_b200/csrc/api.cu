@@ -68,14 +68,27 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Device memory is stream-ordered (cudaMallocAsync on the stream that uses it) from the
+// device's default memory pool, whose release threshold init raises so that freed blocks stay
+// cached: creating and freeing handles per scene costs no cudaMalloc/cudaFree round trips.
 template <typename T>
-void grow(T** ptr, size_t* cap, size_t need, double slack = 1.25) {
+void dalloc(T** ptr, size_t count, cudaStream_t s) {
+    *ptr = nullptr;
+    CK(cudaMallocAsync((void**)ptr, std::max<size_t>(count, 1) * sizeof(T), s));
+}
+
+void dfree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+template <typename T>
+void grow(T** ptr, size_t* cap, size_t need, cudaStream_t s, double slack = 1.25) {
     if (need <= *cap && *ptr) return;
     size_t n = std::max<size_t>(need, (size_t)((double)need * slack));
-    if (*ptr) CK(cudaFree(*ptr));
+    if (*ptr) CK(cudaFreeAsync(*ptr, s));
     *ptr = nullptr;
     *cap = 0;
-    CK(cudaMalloc((void**)ptr, std::max<size_t>(n, 1) * sizeof(T)));
+    dalloc(ptr, n, s);
     *cap = n;
 }
 
@@ -155,15 +168,14 @@ void ctx_init(Ctx& c) {
     CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t)));
 }
 
-void ctx_free(Ctx& c) {
+void ctx_free(Ctx& c, cudaStream_t s) {
     for (auto& es : c.evs)
         for (int k = 0; k < 5; k++) cudaEventDestroy(es.e[k]);
     c.evs.clear();
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect,
                     b.rec0, b.rec1, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, b.bin_count, c.cub_tmp, c.ids_stage};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    for (void* p : ptrs) dfree(p, s);
     if (c.h_total) cudaFreeHost(c.h_total);
     if (c.ev_total) cudaEventDestroy(c.ev_total);
     if (c.s) cudaStreamDestroy(c.s);
@@ -172,21 +184,19 @@ void ctx_free(Ctx& c) {
 
 void ctx_reserve_gaussians(Ctx& c, int64_t G) {
     if ((size_t)G <= c.g_cap && c.vb.depth_key) return;
-    size_t cap = 0;
     ViewBuffers& b = c.vb;
     size_t n = std::max<int64_t>(G, 1);
-#define RG(f) { size_t cc = 0; b.f = nullptr; grow(&b.f, &cc, n, 1.0); }
+#define RG(f) { dalloc(&b.f, n, c.s); }
     if (b.depth_key) {
         void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect, b.rec0, b.rec1};
-        for (void* p : ptrs) CK(cudaFree(p));
+        for (void* p : ptrs) dfree(p, c.s);
     }
     RG(depth_key) RG(depth_key_alt) RG(gidx) RG(gidx_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1)
 #undef RG
-    (void)cap;
     c.g_cap = n;
 }
 
-void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes); }
+void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes, c.s); }
 
 bool rigid_ok(const float* M) {
     double R[3][3];
@@ -310,12 +320,10 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& b
     if (E >= (uint64_t)INT32_MAX)
         return fail(SCOUP_EUNSUPPORTED, "view produces " + std::to_string(E) + " tile entries (>= 2^31)");
     if ((size_t)nbins > c.t_cap || !b.ranges) {
-        if (b.ranges) CK(cudaFree(b.ranges));
-        if (b.bin_count) CK(cudaFree(b.bin_count));
-        b.ranges = nullptr;
-        b.bin_count = nullptr;
-        CK(cudaMalloc((void**)&b.ranges, sizeof(uint2) * nbins));
-        CK(cudaMalloc((void**)&b.bin_count, sizeof(uint32_t) * nbins));
+        dfree(b.ranges, c.s);
+        dfree(b.bin_count, c.s);
+        dalloc(&b.ranges, nbins, c.s);
+        dalloc(&b.bin_count, nbins, c.s);
         c.t_cap = nbins;
     }
     h->host_entries += (int64_t)E;
@@ -323,17 +331,13 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& b
     if (es) CK(cudaEventRecord(es->e[2], c.s));
     if (E > 0) {
         if (E > c.e_cap || !b.ekey) {
-            size_t cap = c.e_cap;
             size_t n = (size_t)((double)E * 1.25);
             void* ptrs[] = {b.ekey, b.eval, b.ekey_alt, b.eval_alt};
-            for (void* p : ptrs)
-                if (p) CK(cudaFree(p));
-            b.ekey = b.eval = b.ekey_alt = b.eval_alt = nullptr;
-            CK(cudaMalloc((void**)&b.ekey, n * 4));
-            CK(cudaMalloc((void**)&b.eval, n * 4));
-            CK(cudaMalloc((void**)&b.ekey_alt, n * 4));
-            CK(cudaMalloc((void**)&b.eval_alt, n * 4));
-            (void)cap;
+            for (void* p : ptrs) dfree(p, c.s);
+            dalloc(&b.ekey, n, c.s);
+            dalloc(&b.eval, n, c.s);
+            dalloc(&b.ekey_alt, n, c.s);
+            dalloc(&b.eval_alt, n, c.s);
             c.e_cap = n;
         }
         CK(cudaMemsetAsync(b.bin_count, 0, sizeof(uint32_t) * nbins, c.s));
@@ -423,26 +427,33 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
         h->L = L;
         h->K = K;
         CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+        {
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t keep = UINT64_MAX;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
+        cudaStream_t hs = h->stream;
         if (W) {
             h->W = W;
             h->Z = Z;
         } else {
-            CK(cudaMalloc((void**)&h->W, sizeof(float) * std::max<int64_t>(1, rows_padded) * L));
-            CK(cudaMalloc((void**)&h->Z, sizeof(float) * std::max<int64_t>(1, rows_padded)));
+            dalloc(&h->W, (size_t)std::max<int64_t>(1, rows_padded) * L, hs);
+            dalloc(&h->Z, (size_t)std::max<int64_t>(1, rows_padded), hs);
             h->own_wz = true;
         }
-        CK(cudaMalloc((void**)&h->d_err_code, sizeof(int)));
-        CK(cudaMalloc((void**)&h->d_err_index, sizeof(long long)));
-        CK(cudaMalloc((void**)&h->d_stats, 5 * sizeof(unsigned long long)));
+        dalloc(&h->d_err_code, 1, hs);
+        dalloc(&h->d_err_index, 1, hs);
+        dalloc(&h->d_stats, 5, hs);
         CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
         CK(cudaMemsetAsync(h->d_err_index, 0, sizeof(long long), h->stream));
         CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->W, 0, sizeof(float) * rows_padded * L, h->stream));
         CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * rows_padded, h->stream));
         const int64_t G = std::max<int64_t>(1, num_gaussians);
-        CK(cudaMalloc((void**)&h->pg.a, sizeof(float4) * G));
-        CK(cudaMalloc((void**)&h->pg.b, sizeof(float4) * G));
-        CK(cudaMalloc((void**)&h->pg.c, sizeof(float2) * G));
+        dalloc(&h->pg.a, G, hs);
+        dalloc(&h->pg.b, G, hs);
+        dalloc(&h->pg.c, G, hs);
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         for (int i = 0; i < 2; i++) {
             CK(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
@@ -458,7 +469,7 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
                     dsrc[k] = src[k];
                 } else {
                     float* d = nullptr;
-                    CK(cudaMalloc((void**)&d, sizeof(float) * cnt[k] * num_gaussians));
+                    dalloc(&d, cnt[k] * num_gaussians, hs);
                     CK(cudaMemcpyAsync(d, src[k], sizeof(float) * cnt[k] * num_gaussians, cudaMemcpyHostToDevice,
                                        h->stream));
                     tmp.push_back(d);
@@ -467,10 +478,10 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
             }
             launch_activate(dsrc[0], dsrc[1], dsrc[2], dsrc[3], num_gaussians, h->pg, latch_of(h), h->stream);
             CK(cudaGetLastError());
-            if (!tmp.empty()) {
-                CK(cudaStreamSynchronize(h->stream));
-                for (float* d : tmp) CK(cudaFree(d));
-            }
+            // host inputs were copied (pageable copies complete before returning; pinned ones
+            // are ordered before the frees below on the same stream)
+            for (float* d : tmp) dfree(d, hs);
+            if (!tmp.empty()) CK(cudaStreamSynchronize(hs));
         }
     } catch (const CudaError& e) {
         scoup_uplift_free(h);
@@ -519,16 +530,15 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             const size_t nslots = (size_t)(rows * S);
             if (nslots > h->code_cap) {
                 size_t cap = (size_t)((double)nslots * 1.25);
-                if (h->code_atoms) CK(cudaFree(h->code_atoms));
-                if (h->code_coefs) CK(cudaFree(h->code_coefs));
-                if (h->code_atoms_in) CK(cudaFree(h->code_atoms_in));
-                if (h->code_coefs_in) CK(cudaFree(h->code_coefs_in));
-                h->code_atoms = nullptr; h->code_coefs = nullptr; h->code_atoms_in = nullptr; h->code_coefs_in = nullptr;
+                dfree(h->code_atoms, h->stream);
+                dfree(h->code_coefs, h->stream);
+                dfree(h->code_atoms_in, h->stream);
+                dfree(h->code_coefs_in, h->stream);
                 h->code_cap = 0;
-                CK(cudaMalloc((void**)&h->code_atoms, sizeof(uint32_t) * cap));
-                CK(cudaMalloc((void**)&h->code_coefs, sizeof(float) * cap));
-                CK(cudaMalloc((void**)&h->code_atoms_in, sizeof(uint32_t) * cap));
-                CK(cudaMalloc((void**)&h->code_coefs_in, sizeof(float) * cap));
+                dalloc(&h->code_atoms, cap, h->stream);
+                dalloc(&h->code_coefs, cap, h->stream);
+                dalloc(&h->code_atoms_in, cap, h->stream);
+                dalloc(&h->code_coefs_in, cap, h->stream);
                 h->code_cap = cap;
             }
             const uint32_t* ain = code_atoms;
@@ -552,7 +562,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
         for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
         auto ids_for = [&](Ctx& c, int v) -> const uint32_t* {
             if (ids_on_device) return region_ids + (int64_t)v * npx;
-            grow(&c.ids_stage, &c.ids_cap, (size_t)npx, 1.0);
+            grow(&c.ids_stage, &c.ids_cap, (size_t)npx, c.s, 1.0);
             CK(cudaMemcpyAsync(c.ids_stage, region_ids + (int64_t)v * npx, sizeof(uint32_t) * npx,
                                cudaMemcpyHostToDevice, c.s));
             return c.ids_stage;
@@ -605,8 +615,8 @@ scoup_status scoup_uplift_finalize_topk(scoup_uplift* h, int64_t first_row, int6
             uint32_t* da = out_atoms;
             float* dc = out_coefs;
             if (!dev_out) {
-                CK(cudaMalloc((void**)&da, sizeof(uint32_t) * num_rows * h->K));
-                CK(cudaMalloc((void**)&dc, sizeof(float) * num_rows * h->K));
+                dalloc(&da, (size_t)num_rows * h->K, h->stream);
+                dalloc(&dc, (size_t)num_rows * h->K, h->stream);
             }
             if (h->timing) {
                 if (!h->topk_ev[0]) {
@@ -628,9 +638,8 @@ scoup_status scoup_uplift_finalize_topk(scoup_uplift* h, int64_t first_row, int6
             if (!dev_out) {
                 CK(cudaMemcpyAsync(out_atoms, da, sizeof(uint32_t) * num_rows * h->K, cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaMemcpyAsync(out_coefs, dc, sizeof(float) * num_rows * h->K, cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaStreamSynchronize(h->stream));
-                CK(cudaFree(da));
-                CK(cudaFree(dc));
+                dfree(da, h->stream);
+                dfree(dc, h->stream);
             }
         }
         CK(cudaStreamSynchronize(h->stream));
@@ -729,7 +738,7 @@ void scoup_uplift_free(scoup_uplift* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (int i = 0; i < 2; i++) {
         if (h->ctx[i].s) cudaStreamSynchronize(h->ctx[i].s);
-        ctx_free(h->ctx[i]);
+        ctx_free(h->ctx[i], h->stream);
         if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
     }
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -737,12 +746,12 @@ void scoup_uplift_free(scoup_uplift* h) {
         if (h->topk_ev[i]) cudaEventDestroy(h->topk_ev[i]);
     void* ptrs[] = {h->pg.a, h->pg.b, h->pg.c, h->d_err_code, h->d_err_index, h->d_stats, h->code_atoms,
                     h->code_coefs, h->code_atoms_in, h->code_coefs_in};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    for (void* p : ptrs) dfree(p, h->stream);
     if (h->own_wz) {
-        cudaFree(h->W);
-        cudaFree(h->Z);
+        dfree(h->W, h->stream);
+        dfree(h->Z, h->stream);
     }
+    cudaStreamSynchronize(h->stream);
     delete h;
 }
 

@@ -1,18 +1,21 @@
 // raster.cu -- fused rasterise-and-aggregate kernel (the hot loop of Algorithm 1).
 //
-// One CTA of 256 threads per 16x16 tile, one pixel per thread (row-major: a warp is a 16x2
-// pixel block).  The tile reads the depth-ordered Gaussian list of the bin that contains it
-// (bins are power-of-two groups of tiles) and walks it front to back:
+// One CTA of 256 threads per 16x16 tile, one pixel per thread; warp w covers the 8x4 pixel
+// block at column 8*(w&1), row 4*(w>>1) of the tile (near-square blocks keep the number of
+// (warp, Gaussian) pairs low for small footprints).  The tile reads the depth-ordered Gaussian
+// list of the bin that contains it (bins are power-of-two groups of tiles) and
+// walks it front to back:
 //
 //  refill   256 candidates at a time are tested against the tile (square support and the
 //           alpha >= 1/255 ellipse, conservatively) and stably compacted into a shared-memory
 //           ring of records, so the ring stays in (depth, index) order;
-//  batch    32 ring records at a time: each warp builds the mask of records whose support
-//           touches its 16x2 block (exact row intervals, conservative margins) and evaluates
-//           only those, in order, per pixel -- DESIGN.md §3 step PX: square test, the
-//           log2-domain quadratic form, the q <= 0 guard, alpha = min(0.99, o exp2_spec(q)),
-//           the alpha >= 1/255 skip and the T(1-alpha) < 1e-4 stop -- giving the weights
-//           e_i(v,p) = alpha_i T of PAPER.md Eq. 2, bit-identical to the CPU oracle.
+//  batch    32 ring records at a time: each warp ballots the records whose support touches
+//           its 8x4 block (conservative) and, in order, every lane evaluates DESIGN.md §3 step
+//           PX on them -- square test, the log2-domain quadratic form, the q <= 0 guard,
+//           alpha = min(0.99, o exp2_spec(q)), the alpha >= 1/255 skip and the T(1-alpha) < 1e-4
+//           stop -- giving the weights e_i(v,p) = alpha_i T of PAPER.md Eq. 2,
+//           bit-identical to the CPU oracle.  Control flow is warp-uniform (one uniform branch
+//           per record); the per-lane decisions are predicates/selects.
 //
 // Aggregation (Eq. 5; Algorithm 1 lines 8-10): per warp and region
 // group, the per-pixel weights of the batch are summed with a 31-shuffle transpose-reduction
@@ -138,9 +141,11 @@ __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* a
 }
 
 struct __align__(16) Smem {
-    float4 q0[QCAP];   // ring of candidate records: (mx, my, r, o)
-    float4 q1[QCAP];   //                            (qa, qb, qc, ycut)
-    uint32_t qg[QCAP]; //                            Gaussian id
+    // ring of candidate records; slots [0, BATCH) are mirrored at [QCAP, QCAP + BATCH) so a
+    // batch q_head .. q_head + BATCH - 1 is always contiguous
+    float4 q0[QCAP + BATCH];   // (mx, my, r, o)
+    float4 q1[QCAP + BATCH];   // (qa, qb, qc, ycut)
+    uint32_t qg[QCAP + BATCH]; // Gaussian id
     float acc[2][MAX_SLOTS * BATCH];
     float accZ[2][BATCH];
     uint32_t slot_key[MAX_SLOTS];
@@ -153,23 +158,27 @@ struct __align__(16) Smem {
     unsigned long long tests;
 };
 
-__global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const RasterParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+#ifndef RASTER_MIN_BLOCKS
+#define RASTER_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_kernel(const RasterParams p) {
+    __shared__ Smem sm;
     const int tile = blockIdx.x;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
     const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
     const uint2 range = p.ranges[bin];
     if (range.x >= range.y) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int x = tx * TILE + (t & (TILE - 1)), y = ty * TILE + (t >> 4);
+    const int wx0 = tx * TILE + 8 * (warp & 1), wy0 = ty * TILE + 4 * (warp >> 1);
+    const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
     const int Wd = p.cam.width, Hd = p.cam.height;
     const bool inside = x < Wd && y < Hd;
-    // pixel-centre rectangles of the tile and of this warp's 16x2 block (clipped to the image)
+    // pixel-centre rectangles of the tile and of this warp's 8x4 block (clipped to the image)
     const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
     const float TX1 = (float)(min(tx * TILE + TILE, Wd) - 1) + 0.5f;
     const float TY1 = (float)(min(ty * TILE + TILE, Hd) - 1) + 0.5f;
-    const float WY0 = (float)(ty * TILE + 2 * warp) + 0.5f, WY1 = WY0 + 1.f;
+    const float WX0 = (float)wx0 + 0.5f, WY0 = (float)wy0 + 0.5f;
+    const float WX1 = (float)(min(wx0 + 8, Wd) - 1) + 0.5f, WY1 = (float)(min(wy0 + 4, Hd) - 1) + 0.5f;
 
     // ---- setup: region key of my pixel, tile slot table, slot codes
     uint32_t key = KEY_NONE;
@@ -220,8 +229,9 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
     const int64_t my_code_row = (p.code_row0 + (int64_t)(coded ? key : 0)) * S;
 
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
-    float T = 1.0f;
-    bool done = !inside;
+    // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
+    // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
+    float T = inside ? 1.0f : 0.0f;
     uint32_t cnt = 0, tests = 0;
     float* Wm = p.W;
     const int L = p.L;
@@ -258,6 +268,11 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                 sm.qg[pos] = g;
                 sm.q0[pos] = r0;
                 sm.q1[pos] = r1;
+                if (pos < (uint32_t)BATCH) {
+                    sm.qg[pos + QCAP] = g;
+                    sm.q0[pos + QCAP] = r0;
+                    sm.q1[pos + QCAP] = r1;
+                }
             }
             q_count += tot;
             cursor += TILE_PIX;
@@ -267,62 +282,50 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
         const uint32_t n = min((uint32_t)BATCH, q_count);
 
         // ---- per-warp mask of batch records touching this warp's 16x2 block
-        const bool warp_done = __all_sync(FULL, done);
+        const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
         if (!warp_done && (uint32_t)lane < n) {
-            const uint32_t pos = (q_head + lane) & (QCAP - 1);
-            rel = rect_relevant(sm.q0[pos], sm.q1[pos], TX0, TX1, WY0, WY1);
+            rel = rect_relevant(sm.q0[q_head + lane], sm.q1[q_head + lane], WX0, WX1, WY0, WY1);
         }
         const unsigned mask = __ballot_sync(FULL, rel);
 
-        // ---- rasterise: e[i] for the i-th relevant record, in depth order (DESIGN.md §3 PX)
+        // ---- rasterise: e[j] for batch record j, in depth order (DESIGN.md §3 PX).  The branch
+        // on `mask` is warp-uniform; every lane computes the full sequence and the per-pixel
+        // decisions select the result (records outside the square or already-done pixels
+        // leave e[j] = 0 and T unchanged).
         float e[BATCH];
+        uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
+        const float4* b0 = sm.q0 + q_head;
+        const float4* b1 = sm.q1 + q_head;
 #pragma unroll
-        for (int i = 0; i < BATCH; i++) e[i] = 0.f;
-        bool any = false;
-        unsigned m = mask;
-#pragma unroll
-        for (int i = 0; i < BATCH; i++) {
-            if (m == 0u) break;
-            const int j = __ffs(m) - 1;
-            m &= m - 1u;
-            if (!done) {
-                const uint32_t pos = (q_head + j) & (QCAP - 1);
-                const float4 a = sm.q0[pos];  // mx, my, r, o
+        for (int j = 0; j < BATCH; j++) {
+            e[j] = 0.f;
+            if (mask & (1u << j)) {
+                const float4 a = b0[j];  // mx, my, r, o
+                const float4 b = b1[j];  // qa, qb, qc, ycut
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
-                if (fabsf(dx) <= a.z && fabsf(dy) <= a.z) {
-                    tests++;
-                    const float4 b = sm.q1[pos];  // qa, qb, qc, ycut
-                    const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
-                                              __fmul_rn(__fmul_rn(b.z, dy), dy));
-                    if (!(q > 0.f) && q >= b.w) {
-                        const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
-                        if (al >= K_AMIN) {
-                            const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
-                            if (Tn < K_TMIN) {
-                                done = true;
-                            } else {
-                                const float ev = __fmul_rn(al, T);
-                                e[i] = ev;
-                                T = Tn;
-                                cnt++;
-                                any = true;
-                            }
-                        }
-                    }
-                }
+                const bool sq = T > 0.f && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
+                                          __fmul_rn(__fmul_rn(b.z, dy), dy));
+                const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
+                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
+                const bool pass = sq && !(q > 0.f) && q >= b.w && al >= K_AMIN;
+                const bool con = pass && !(Tn < K_TMIN);
+                e[j] = con ? __fmul_rn(al, T) : 0.f;
+                T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
+                cbits |= con ? (1u << j) : 0u;
+                tbits |= sq ? (1u << j) : 0u;
             }
         }
+        const bool any = cbits != 0u;
+        cnt += __popc(cbits);
+        tests += __popc(tbits);
         if (overflow && any) {
             // per-pixel reductions straight from the code table (tiles with > MAX_SLOTS regions)
-            unsigned m2 = mask;
 #pragma unroll
-            for (int i = 0; i < BATCH; i++) {
-                if (m2 == 0u) break;
-                const int j = __ffs(m2) - 1;
-                m2 &= m2 - 1u;
-                if (e[i] > 0.f)
-                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, sm.qg[(q_head + j) & (QCAP - 1)], e[i],
+            for (int j = 0; j < BATCH; j++) {
+                if (e[j] > 0.f)
+                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, sm.qg[q_head + j], e[j],
                                   coded ? my_code_row : -1);
             }
         }
@@ -330,14 +333,13 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
         if (!overflow) {
             // ---- per (warp, region group) transpose-reduction, then shared accumulation
             if (__any_sync(FULL, any)) {
+                // lane l ends with the group's sum for batch record l
                 const bool mine_rel = (mask >> lane) & 1u;
-                const int rank = __popc(mask & lanemask_lt);
                 if (grp == FULL) {
                     const float v = transpose_reduce<false>(e, true, lane);
-                    const float vj = __shfl_sync(FULL, v, rank & 31);
-                    if (mine_rel && vj != 0.f) {
-                        atomicAdd(&sm.acc[buf][slot * BATCH + lane], vj);
-                        atomicAdd(&sm.accZ[buf][lane], vj);
+                    if (mine_rel && v != 0.f) {
+                        atomicAdd(&sm.acc[buf][slot * BATCH + lane], v);
+                        atomicAdd(&sm.accZ[buf][lane], v);
                     }
                 } else {
                     float zsum = 0.f;
@@ -348,9 +350,8 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                         const int q = __shfl_sync(FULL, slot, l);
                         todo &= ~g2;
                         const float v = transpose_reduce<true>(e, (g2 >> lane) & 1u, lane);
-                        const float vj = __shfl_sync(FULL, v, rank & 31);
-                        if (mine_rel && vj != 0.f) atomicAdd(&sm.acc[buf][q * BATCH + lane], vj);
-                        zsum += mine_rel ? vj : 0.f;
+                        if (mine_rel && v != 0.f) atomicAdd(&sm.acc[buf][q * BATCH + lane], v);
+                        zsum += mine_rel ? v : 0.f;
                     }
                     if (zsum != 0.f) atomicAdd(&sm.accZ[buf][lane], zsum);
                 }
@@ -365,21 +366,21 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
                 const float v = sm.acc[buf][q * BATCH + j];
                 const uint32_t a = sm.slot_atom[q][s];
                 if (v > 0.f && a != NONE)
-                    atomicAdd(Wm + (int64_t)sm.qg[(q_head + j) & (QCAP - 1)] * L + a,
+                    atomicAdd(Wm + (int64_t)sm.qg[q_head + j] * L + a,
                               __fmul_rn(sm.slot_coef[q][s], v));
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
-                if (z > 0.f) atomicAdd(p.Z + sm.qg[(q_head + t) & (QCAP - 1)], z);
+                if (z > 0.f) atomicAdd(p.Z + sm.qg[q_head + t], z);
             }
             // zero the other accumulator buffer (flushed one batch ago)
             for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[buf ^ 1][i] = 0.f;
             if (t < BATCH) sm.accZ[buf ^ 1][t] = 0.f;
         }
-        q_head += n;
+        q_head = (q_head + n) & (QCAP - 1);
         q_count -= n;
         buf ^= 1;
-        if (__syncthreads_count(!done) == 0) break;  // B2
+        if (__syncthreads_count(T > 0.f) == 0) break;  // B2
     }
 
     // contributions (terms of Eq. 5's sum) and support tests
@@ -402,8 +403,8 @@ __global__ void __launch_bounds__(TILE_PIX, 3) raster_aggregate_kernel(const Ras
 void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
     if (ntiles <= 0) return;
-    static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the default 48 KB window");
-    raster_aggregate_kernel<<<ntiles, TILE_PIX, sizeof(Smem), s>>>(p);
+    static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the static 48 KB window");
+    raster_aggregate_kernel<<<ntiles, TILE_PIX, 0, s>>>(p);
 }
 
 }  // namespace scoup
