@@ -269,8 +269,10 @@ def main():
     alu_peak = sms * 128 * sm_max * 1e6 / 1e12  # T lane-ops/s
     launches = max(1, tm["raster_launches"])
     ras_avg_s = tm["raster_ms"] / launches / 1e3
-    ops_per_launch = (OPS_PER_TEST * st["support_tests"] + (2 * cfg.S + 1) * st["contributions"]) / max(1, st["views"])
-    achieved = ops_per_launch / ras_avg_s / 1e12 if ras_avg_s > 0 else 0.0
+    # algorithmic lane-ops of one step (DESIGN.md §5 a4) over the raster time of one step
+    ops_step = OPS_PER_TEST * st["support_tests"] + (2 * cfg.S + 1) * st["contributions"]
+    ras_step_s = tm["raster_ms"] / args.steps / 1e3
+    achieved = ops_step / ras_step_s / 1e12 if ras_step_s > 0 else 0.0
     total_dev_ms = tm["preprocess_ms"] + tm["binning_ms"] + tm["raster_ms"] + tm["topk_ms"]
 
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
@@ -335,6 +337,7 @@ def main():
             "roofline": {"bound": "alu", "kernel": "raster_aggregate_kernel", "achieved": achieved,
                          "peak": alu_peak, "unit": "T lane-ops/s", "frac": achieved / alu_peak,
                          "traffic": None, "avg_launch_ms": ras_avg_s * 1e3,
+                         "views_per_launch": tm["views_timed"] / launches,
                          "share_of_step": tm["raster_ms"] / max(1e-9, total_dev_ms),
                          "peak_source": f"{sms} SMs x 128 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
             "gpu_launches": int((st["kernel_launches"] + st["cub_launches"]) / max(1, args.steps)),

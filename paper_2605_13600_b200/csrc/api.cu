@@ -15,6 +15,7 @@
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -92,6 +93,8 @@ void grow(T** ptr, size_t* cap, size_t need, cudaStream_t s, double slack = 1.25
     *cap = n;
 }
 
+// One pipeline context: the buffers of one view batch and the stream it runs on.  Two
+// contexts alternate so that batch b+1's projection and depth sort overlap batch b's raster.
 struct Ctx {
     cudaStream_t s = nullptr;
     cudaEvent_t ev_total = nullptr;
@@ -99,14 +102,15 @@ struct Ctx {
     size_t g_cap = 0, e_cap = 0, t_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_cap = 0;
-    uint64_t* h_total = nullptr;  // pinned
+    uint64_t* h_total = nullptr;  // pinned [MAX_VB]: offsets at the end of each view
     uint32_t* ids_stage = nullptr;
     size_t ids_cap = 0;
-    // per-view launch state for stage 2
-    int view = -1;
-    const uint32_t* ids_dev = nullptr;
+    // launch state of the batch in flight (stage 1 done, stage 2 pending)
+    int v0 = 0, nv = 0;
+    int key_bits = 32;
+    const uint32_t* ids_dev[MAX_VB] = {};
     // timing: ring of event sets (start/end of stage 1, binning start, raster start/end)
-    struct EvSet { cudaEvent_t e[5]; bool pending; };
+    struct EvSet { cudaEvent_t e[5]; bool pending; int views; };
     std::vector<EvSet> evs;
     int ev_next = 0;
     int ev_cur = -1;
@@ -143,6 +147,7 @@ struct scoup_uplift {
     cudaEvent_t topk_ev[2] = {nullptr, nullptr};
     bool topk_pending = false;
     int64_t kernel_launches = 0, cub_launches = 0;
+    double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
 };
 
 namespace {
@@ -156,6 +161,8 @@ scoup_status check_latched(scoup_uplift* h) {
     if (code == ERR_NONE) return SCOUP_OK;
     CK(cudaMemcpy(&idx, h->d_err_index, sizeof(long long), cudaMemcpyDeviceToHost));
     h->latched = true;
+    if (code == ERR_DEPTHKEY)
+        return fail(SCOUP_ECUDA, "internal error: depth code beyond the batch bound at batch index " + std::to_string(idx));
     const char* what = code == ERR_GAUSSIAN ? "non-finite or invalid Gaussian parameters at Gaussian index "
                        : code == ERR_REGION ? "region id >= num_regions at flat pixel index "
                                             : "invalid code slot (atom >= L or bad coefficient) at flat slot index ";
@@ -165,7 +172,7 @@ scoup_status check_latched(scoup_uplift* h) {
 void ctx_init(Ctx& c) {
     CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c.ev_total, cudaEventDisableTiming));
-    CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t)));
+    CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t) * MAX_VB));
 }
 
 void ctx_free(Ctx& c, cudaStream_t s) {
@@ -173,8 +180,9 @@ void ctx_free(Ctx& c, cudaStream_t s) {
         for (int k = 0; k < 5; k++) cudaEventDestroy(es.e[k]);
     c.evs.clear();
     ViewBuffers& b = c.vb;
-    void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect,
-                    b.rec0, b.rec1, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, b.bin_count, c.cub_tmp, c.ids_stage};
+    void* ptrs[] = {b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, b.tiles, b.offsets, b.rect,
+                    b.rec0, b.rec1, b.rec2, b.totals, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, b.bin_count,
+                    c.cub_tmp, c.ids_stage};
     for (void* p : ptrs) dfree(p, s);
     if (c.h_total) cudaFreeHost(c.h_total);
     if (c.ev_total) cudaEventDestroy(c.ev_total);
@@ -182,18 +190,21 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     c = Ctx{};
 }
 
-void ctx_reserve_gaussians(Ctx& c, int64_t G) {
-    if ((size_t)G <= c.g_cap && c.vb.depth_key) return;
+// Per-(view, Gaussian) buffers for a batch of n = B*G elements.
+void ctx_reserve_gaussians(Ctx& c, int64_t n) {
+    if ((size_t)n <= c.g_cap && c.vb.depth_key) return;
     ViewBuffers& b = c.vb;
-    size_t n = std::max<int64_t>(G, 1);
-#define RG(f) { dalloc(&b.f, n, c.s); }
+    n = std::max<int64_t>(n, 1);
+#define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
     if (b.depth_key) {
-        void* ptrs[] = {b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, b.tiles, b.offsets, b.rect, b.rec0, b.rec1};
+        void* ptrs[] = {b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, b.tiles, b.offsets, b.rect, b.rec0, b.rec1,
+                        b.rec2};
         for (void* p : ptrs) dfree(p, c.s);
     }
-    RG(depth_key) RG(depth_key_alt) RG(gidx) RG(gidx_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1)
+    RG(depth_key) RG(depth_key_alt) RG(dval) RG(dval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1) RG(rec2)
 #undef RG
-    c.g_cap = n;
+    if (!b.totals) dalloc(&b.totals, MAX_VB, c.s);
+    c.g_cap = (size_t)n;
 }
 
 void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes, c.s); }
@@ -243,7 +254,7 @@ void ev_accumulate(scoup_uplift* h, Ctx::EvSet& es) {
     h->t_bin += b;
     h->t_ras += c;
     h->ras_launches++;
-    h->views_timed++;
+    h->views_timed += es.views;
     es.pending = false;
 }
 
@@ -289,36 +300,80 @@ Binning choose_binning(int Wd, int Hd) {
     return b;
 }
 
-void stage1(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& bn) {
+// Depth-code width for a batch: visible keys are bits(t_z) - bits(0.2f) in [1, bits(bound) -
+// bits(0.2f)], with `bound` an upper bound of t_z over the scene box for every camera of the
+// batch (exact max of the linear map over the box's corners, fp64, padded).  The code must
+// leave the all-ones value free for invisible Gaussians.
+int depth_key_bits(const scoup_uplift* h, const Camera* cams, int n) {
+    double zmax = 0.2;
+    for (int v = 0; v < n; v++) {
+        const float* P = cams[v].P;
+        for (int corner = 0; corner < 8; corner++) {
+            const double x = (corner & 1) ? h->bb[3] : h->bb[0], y = (corner & 2) ? h->bb[4] : h->bb[1],
+                         z = (corner & 4) ? h->bb[5] : h->bb[2];
+            zmax = std::max(zmax, (double)P[8] * x + (double)P[9] * y + (double)P[10] * z + (double)P[11]);
+        }
+    }
+    const double bound = zmax * (1.0 + 1e-4) + 1e-4;
+    if (!(bound < 3.0e38)) return 32;
+    const float bf = (float)bound;
+    uint32_t bbits, nbits;
+    std::memcpy(&bbits, &bf, 4);
+    const float nearf = 0.2f;
+    std::memcpy(&nbits, &nearf, 4);
+    const uint64_t need = (uint64_t)(bbits - nbits) + 2;  // largest visible code + the none code
+    int k = 1;
+    while (k < 32 && (1ull << k) < need) k++;
+    return k;
+}
+
+// Stage 1 of a view batch: preprocess (all B views in one launch), one stable radix sort of
+// the (view, depth) keys, scan of the bin counts in that order -> per-view entry totals
+// (async to pinned host).
+void stage1(scoup_uplift* h, Ctx& c, const Camera* cams, int nv, const Binning& bn) {
     const int64_t G = h->G;
+    const int64_t n = (int64_t)nv * G;
     ViewBuffers& b = c.vb;
+    CamBatch cb{};
+    cb.n = nv;
+    for (int v = 0; v < nv; v++) cb.cam[v] = cams[v];
+    int vbits = 0;
+    while ((1 << vbits) < nv) vbits++;
+    const int kb = vbits == 0 ? 32 : c.key_bits;  // single view: full 32-bit code
+    const int end_bit = vbits == 0 ? 32 : kb + vbits;
     Ctx::EvSet* es = ev_begin(h, c);
-    if (es) CK(cudaEventRecord(es->e[0], c.s));
-    launch_preprocess(h->pg, G, cam, bn, b, h->d_stats + 3, c.s);
+    if (es) { CK(cudaEventRecord(es->e[0], c.s)); es->views = nv; }
+    launch_preprocess(h->pg, G, cb, bn, b, kb, h->d_stats + 3, latch_of(h), c.s);
     size_t need = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, (int)G, 0, 32, c.s));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, (int)n, 0,
+                                       end_bit, c.s));
     size_t need2 = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)G, c.s));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)n, c.s));
     ctx_reserve_cub(c, std::max(need, need2));
-    CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.depth_key, b.depth_key_alt, b.gidx, b.gidx_sorted, (int)G, 0, 32, c.s));
-    launch_gather_scan_input(b.gidx_sorted, b.tiles, b.offsets, G, c.s);
-    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)G, c.s));
-    CK(cudaMemcpyAsync(c.h_total, b.offsets + (G - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, (int)n,
+                                       0, end_bit, c.s));
+    launch_gather_scan_input(b.dval_sorted, b.tiles, b.offsets, n, c.s);
+    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)n, c.s));
+    launch_view_totals(b.offsets, G, nv, b.totals, c.s);
+    CK(cudaMemcpyAsync(c.h_total, b.totals, sizeof(uint64_t) * nv, cudaMemcpyDeviceToHost, c.s));
     if (es) CK(cudaEventRecord(es->e[1], c.s));
     CK(cudaEventRecord(c.ev_total, c.s));
-    h->kernel_launches += 2;
+    h->kernel_launches += 3;
     h->cub_launches += 2;
 }
 
-// Stage 2: emit, tile sort, ranges, raster.  Requires stage 1's total on the host.
-scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& bn, const uint32_t* ids,
-                    int64_t code_row0, int32_t num_regions, int S, long long* contrib_out, long long pixel_base) {
+// Stage 2 of a view batch: emit, bin sort, ranges, raster.  Needs stage 1's totals on the host.
+scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera* cams, const Binning& bn, const int64_t* code_row0,
+                    const int32_t* num_regions, int S, long long* contrib_out, int64_t npx) {
     CK(cudaEventSynchronize(c.ev_total));
-    const uint64_t E = *c.h_total;
-    const int nbins = bn.nbins();
+    const int nv = c.nv;
+    const int64_t G = h->G;
+    const int64_t n = (int64_t)nv * G;
+    const uint64_t E = c.h_total[nv - 1];
+    const int nbins = bn.nbins() * nv;
     ViewBuffers& b = c.vb;
     if (E >= (uint64_t)INT32_MAX)
-        return fail(SCOUP_EUNSUPPORTED, "view produces " + std::to_string(E) + " tile entries (>= 2^31)");
+        return fail(SCOUP_EUNSUPPORTED, "view batch produces " + std::to_string(E) + " bin entries (>= 2^31)");
     if ((size_t)nbins > c.t_cap || !b.ranges) {
         dfree(b.ranges, c.s);
         dfree(b.bin_count, c.s);
@@ -331,17 +386,17 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& b
     if (es) CK(cudaEventRecord(es->e[2], c.s));
     if (E > 0) {
         if (E > c.e_cap || !b.ekey) {
-            size_t n = (size_t)((double)E * 1.25);
+            size_t ne = (size_t)((double)E * 1.25);
             void* ptrs[] = {b.ekey, b.eval, b.ekey_alt, b.eval_alt};
             for (void* p : ptrs) dfree(p, c.s);
-            dalloc(&b.ekey, n, c.s);
-            dalloc(&b.eval, n, c.s);
-            dalloc(&b.ekey_alt, n, c.s);
-            dalloc(&b.eval_alt, n, c.s);
-            c.e_cap = n;
+            dalloc(&b.ekey, ne, c.s);
+            dalloc(&b.eval, ne, c.s);
+            dalloc(&b.ekey_alt, ne, c.s);
+            dalloc(&b.eval_alt, ne, c.s);
+            c.e_cap = ne;
         }
         CK(cudaMemsetAsync(b.bin_count, 0, sizeof(uint32_t) * nbins, c.s));
-        launch_emit(b.gidx_sorted, b.offsets, b.rect, bn, h->G, b.ekey, b.eval, b.bin_count, c.s);
+        launch_emit(b.dval_sorted, b.offsets, b.rect, bn, n, G, b.ekey, b.eval, b.bin_count, c.s);
         launch_ranges_from_counts(b.bin_count, nbins, b.ranges, c.s);
         const int nbits = bits_for((uint32_t)nbins);
         size_t need = 0;
@@ -349,26 +404,33 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera& cam, const Binning& b
         ctx_reserve_cub(c, need);
         CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
         RasterParams p{};
-        p.cam = cam;
+        p.nviews = nv;
+        p.width = cams[0].width;
+        p.height = cams[0].height;
+        p.G = G;
         p.bn = bn;
         p.ranges = b.ranges;
         p.eval = b.eval_alt;
         p.rec0 = b.rec0;
         p.rec1 = b.rec1;
-        p.region_ids = ids;
+        p.rec2 = b.rec2;
+        for (int v = 0; v < nv; v++) {
+            const int u = c.v0 + v;
+            p.region_ids[v] = c.ids_dev[v];
+            p.code_row0[v] = code_row0[u];
+            p.num_regions[v] = num_regions[u];
+            p.pixel_base[v] = (long long)u * npx;
+            p.contrib_out[v] = contrib_out ? contrib_out + u : nullptr;
+        }
         p.code_atoms = h->code_atoms;
         p.code_coefs = h->code_coefs;
-        p.code_row0 = code_row0;
-        p.num_regions = num_regions;
         p.S = S;
         p.L = h->L;
         p.W = h->W;
         p.Z = h->Z;
         p.contrib_ctr = h->d_stats + 1;
-        p.contrib_out = contrib_out;
-        p.err = latch_of(h);
-        p.pixel_base = pixel_base;
         p.support_ctr = h->d_stats + 4;
+        p.err = latch_of(h);
         if (es) CK(cudaEventRecord(es->e[3], c.s));
         launch_raster(p, c.s);
         h->kernel_launches += 3;
@@ -478,6 +540,22 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
             }
             launch_activate(dsrc[0], dsrc[1], dsrc[2], dsrc[3], num_gaussians, h->pg, latch_of(h), h->stream);
             CK(cudaGetLastError());
+            // scene box (for the depth-code width of each view batch)
+            int* dbox = nullptr;
+            dalloc(&dbox, 6, hs);
+            const int init_box[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+            CK(cudaMemcpyAsync(dbox, init_box, sizeof(init_box), cudaMemcpyHostToDevice, hs));
+            launch_bounds(h->pg, num_gaussians, dbox, hs);
+            int box[6];
+            CK(cudaMemcpyAsync(box, dbox, sizeof(box), cudaMemcpyDeviceToHost, hs));
+            CK(cudaStreamSynchronize(hs));
+            dfree(dbox, hs);
+            for (int a = 0; a < 6; a++) {
+                const int bits = box[a] >= 0 ? box[a] : box[a] ^ 0x7FFFFFFF;
+                float f;
+                std::memcpy(&f, &bits, 4);
+                h->bb[a] = (box[0] > box[3]) ? 0.0 : (double)f;  // no valid Gaussian: empty box
+            }
             // host inputs were copied (pageable copies complete before returning; pinned ones
             // are ordered before the frees below on the same stream)
             for (float* d : tmp) dfree(d, hs);
@@ -552,34 +630,40 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             launch_ingest_codes(ain, cin, rows, S, h->K, h->L, h->code_atoms, h->code_coefs, latch_of(h), h->stream);
         }
         const bool ids_on_device = is_device_ptr(region_ids);
-        // ---- fork the two view contexts off the caller's stream
+        // ---- view batches: B views per pass (bounded by the bin-table size)
+        const int B = std::max(1, std::min(MAX_VB, std::min(MAX_BINS / bn.nbins(), (int)num_views)));
+        // ---- fork the two pipeline contexts off the caller's stream
         CK(cudaEventRecord(h->ev_fork, h->stream));
         for (int i = 0; i < 2; i++) {
             CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
-            ctx_reserve_gaussians(h->ctx[i], h->G);
+            ctx_reserve_gaussians(h->ctx[i], (int64_t)B * h->G);
         }
         std::vector<Camera> cams(num_views);
         for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
-        auto ids_for = [&](Ctx& c, int v) -> const uint32_t* {
-            if (ids_on_device) return region_ids + (int64_t)v * npx;
-            grow(&c.ids_stage, &c.ids_cap, (size_t)npx, c.s, 1.0);
-            CK(cudaMemcpyAsync(c.ids_stage, region_ids + (int64_t)v * npx, sizeof(uint32_t) * npx,
-                               cudaMemcpyHostToDevice, c.s));
-            return c.ids_stage;
-        };
+        const int nbatch = (num_views + B - 1) / B;
         scoup_status st = SCOUP_OK;
-        for (int v = 0; v <= num_views && st == SCOUP_OK; v++) {
-            if (v < num_views) {
-                Ctx& c = h->ctx[v & 1];
-                c.view = v;
-                c.ids_dev = ids_for(c, v);
-                stage1(h, c, cams[v], bn);
+        for (int bi = 0; bi <= nbatch && st == SCOUP_OK; bi++) {
+            if (bi < nbatch) {
+                Ctx& c = h->ctx[bi & 1];
+                c.v0 = bi * B;
+                c.nv = std::min(B, num_views - c.v0);
+                c.key_bits = depth_key_bits(h, &cams[c.v0], c.nv);
+                if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(B * npx), c.s, 1.0);
+                for (int v = 0; v < c.nv; v++) {
+                    const int u = c.v0 + v;
+                    if (ids_on_device) {
+                        c.ids_dev[v] = region_ids + (int64_t)u * npx;
+                    } else {
+                        CK(cudaMemcpyAsync(c.ids_stage + (int64_t)v * npx, region_ids + (int64_t)u * npx,
+                                           sizeof(uint32_t) * npx, cudaMemcpyHostToDevice, c.s));
+                        c.ids_dev[v] = c.ids_stage + (int64_t)v * npx;
+                    }
+                }
+                stage1(h, c, &cams[c.v0], c.nv, bn);
             }
-            if (v > 0) {
-                Ctx& c = h->ctx[(v - 1) & 1];
-                const int u = v - 1;
-                st = stage2(h, c, cams[u], bn, c.ids_dev, code_row0[u], num_regions[u], S,
-                            contributions_out ? (long long*)contributions_out + u : nullptr, (long long)u * npx);
+            if (bi > 0) {
+                Ctx& c = h->ctx[(bi - 1) & 1];
+                st = stage2(h, c, &cams[c.v0], bn, code_row0, num_regions, S, (long long*)contributions_out, npx);
             }
         }
         // ---- join back into the caller's stream

@@ -6,6 +6,10 @@
 //   ranges          per-tile [begin, end) of the tile-sorted entries
 //   ingest_codes    Algorithm 1's per-pixel TopK(W_v(p)) realised per region
 //   topk            Eq. 6 Top-K + L1 renormalisation (Algorithm 1)
+#include <climits>
+
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace scoup {
@@ -73,14 +77,53 @@ __global__ void activate_kernel(const float* __restrict__ means, const float* __
     pg.c[i] = make_float2(V[4], V[5]);
 }
 
-// ------------------------------------------------------------------ preprocess (V1-V7)
-__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, Camera cam, Binning bn,
-                                                         ViewBuffers vb, unsigned long long* visible_ctr) {
+// ------------------------------------------------------------------ scene bounds
+// Axis-aligned box of the valid means (init): the host derives each view batch's depth bound
+// from it, hence how many bits the depth code needs.  Floats are mapped to order-preserving
+// ints for atomicMin/Max.
+__device__ __forceinline__ int ord_int(float f) {
+    int b = __float_as_int(f);
+    return b >= 0 ? b : b ^ 0x7FFFFFFF;
+}
+
+__global__ void bounds_kernel(PackedGaussians pg, int64_t G, int* bbox) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 A = pg.a[i];
+        if (A.w < 0.f) continue;  // invalid Gaussian (latched at init)
+        const int v[3] = {ord_int(A.x), ord_int(A.y), ord_int(A.z)};
+#pragma unroll
+        for (int a = 0; a < 3; a++) { lo[a] = min(lo[a], v[a]); hi[a] = max(hi[a], v[a]); }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) { atomicMin(bbox + a, lo[a]); atomicMax(bbox + 3 + a, hi[a]); }
+    }
+}
+
+// ------------------------------------------------------------------ preprocess (V1-V7)
+// One thread per (view, Gaussian): grid.y = view of the batch.  Writes the per-view records at
+// batch index j = v*G + i and the sort key (v << key_bits) | (bits(t_z) - bits(0.2f)), which
+// orders (view, depth) exactly (positive floats order as their bit patterns; the stable sort
+// keeps index order on ties); invisible Gaussians get the view's all-ones code.
+__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                         Binning bn, ViewBuffers vb, int key_bits,
+                                                         unsigned long long* visible_ctr, ErrorLatch err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int view = blockIdx.y;
+    const Camera& cam = cams.cam[view];
+    const int64_t j = (int64_t)view * G + i;
+    const uint32_t code_none = (key_bits >= 32) ? 0xFFFFFFFFu : ((1u << key_bits) - 1u);
     bool vis = false;
     if (i < G) {
         float4 A = pg.a[i];
-        uint32_t key = NONE, ntiles = 0;
+        uint32_t key = code_none, ntiles = 0;
         const float o = A.w;
         // V1: camera-space mean
         float t[3];
@@ -169,53 +212,65 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                     int y0 = (int)fmaxf(fy0, 0.f), y1 = (int)fminf(fy1, Hm1);
                     int tx0 = x0 >> bn.bshx, tx1 = (x1 >> bn.bshx) + 1, ty0 = y0 >> bn.bshy, ty1 = (y1 >> bn.bshy) + 1;
                     ntiles = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
-                    key = __float_as_uint(t[2]);
-                    vb.rect[i] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
-                    vb.rec0[i] = make_float4(mx, my, r, o);
-                    vb.rec1[i] = make_float4(qa, qb, qc, ycut);
+                    key = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);  // >= 1 (t_z > 0.2f)
+                    if (key >= code_none) {  // beyond the host's depth bound (cannot happen)
+                        latch_error(err, ERR_DEPTHKEY, j);
+                        key = code_none - 1u;
+                    }
+                    vb.rect[j] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
+                    vb.rec0[j] = make_float4(mx, my, r, o);
+                    vb.rec1[j] = make_float4(qa, qb, qc, ycut);
+                    vb.rec2[j] = make_float2(hx + padx, hy + pady);
                     vis = true;
                 }
             }
         }
-        vb.depth_key[i] = key;
-        vb.tiles[i] = ntiles;
-        vb.gidx[i] = (uint32_t)i;
+        vb.depth_key[j] = key_bits >= 32 ? key : (((uint32_t)view << key_bits) | key);
+        vb.tiles[j] = ntiles;
+        vb.dval[j] = (uint32_t)j;
     }
     unsigned ballot = __ballot_sync(0xffffffffu, vis);
     if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(visible_ctr, (unsigned long long)__popc(ballot));
 }
 
-__global__ void gather_tiles_kernel(const uint32_t* __restrict__ gidx_sorted, const uint32_t* __restrict__ tiles,
-                                    uint64_t* __restrict__ out, int64_t G) {
+__global__ void gather_tiles_kernel(const uint32_t* __restrict__ dval_sorted, const uint32_t* __restrict__ tiles,
+                                    uint64_t* __restrict__ out, int64_t n) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < G) out[k] = tiles[gidx_sorted[k]];
+    if (k < n) out[k] = tiles[dval_sorted[k]];
+}
+
+// totals[v] = inclusive offset at the end of view v's sorted segment [v*G, (v+1)*G)
+__global__ void view_totals_kernel(const uint64_t* __restrict__ offsets, int64_t G, int nviews,
+                                   uint64_t* __restrict__ totals) {
+    const int v = threadIdx.x;
+    if (v < nviews) totals[v] = G > 0 ? offsets[(int64_t)(v + 1) * G - 1] : 0ull;
 }
 
 // ------------------------------------------------------------------ emit
-// Entry m of the Gaussian at depth position k goes to slot offsets[k-1] + m, so the
-// entries are in (depth, index) order before the stable bin sort.  Per-bin entry counts are
-// accumulated through a shared-memory histogram (they give the bin ranges directly).
-constexpr int MAX_BINS = 1024;
-
-__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ gidx_sorted,
+// Entry m of the element at sorted position k (view v = k / G) goes to slot offsets[k-1] + m
+// with key v*nbins + bin, so the entries are in (view, depth, index) order before the stable
+// bin sort.  Per-bin entry counts are accumulated through a shared-memory histogram (they give
+// the bin ranges directly).
+__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ dval_sorted,
                                                    const uint64_t* __restrict__ offsets,
-                                                   const uint2* __restrict__ rect, int bins_x, int nbins, int64_t G,
-                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
-                                                   uint32_t* __restrict__ bin_count) {
+                                                   const uint2* __restrict__ rect, int bins_x, int nbins, int64_t n,
+                                                   int64_t G, uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
+                                                   uint32_t* __restrict__ bin_count, int total_bins) {
     __shared__ uint32_t hist[MAX_BINS];
-    for (int i = threadIdx.x; i < nbins; i += blockDim.x) hist[i] = 0;
+    for (int i = threadIdx.x; i < total_bins; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint64_t begin = 0, end = 0;
-    uint32_t g = 0;
+    uint32_t g = 0, kbase = 0;
     uint2 rc = make_uint2(0, 0);
-    if (k < G) {
+    if (k < n) {
         begin = k > 0 ? offsets[k - 1] : 0;
         end = offsets[k];
         if (end > begin) {
-            g = gidx_sorted[k];
+            g = dval_sorted[k];
             rc = rect[g];
+            kbase = (uint32_t)(k / G) * (uint32_t)nbins;
         }
     }
     const uint32_t cnt = (uint32_t)(end - begin);
@@ -223,7 +278,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     if (cnt > 0 && cnt <= SMALL) {
         const uint32_t bx0 = rc.x & 0xFFFFu, by0 = rc.x >> 16, w = (rc.y & 0xFFFFu) - bx0;
         for (uint32_t m = 0; m < cnt; m++) {
-            const uint32_t key = (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
+            const uint32_t key = kbase + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
             ekey[begin + m] = key;
             eval[begin + m] = g;
             atomicAdd(&hist[key], 1u);
@@ -237,34 +292,38 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
         const uint32_t rx = __shfl_sync(0xffffffffu, rc.x, src), ry = __shfl_sync(0xffffffffu, rc.y, src);
         const uint64_t sb = __shfl_sync(0xffffffffu, begin, src);
         const uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
+        const uint32_t skb = __shfl_sync(0xffffffffu, kbase, src);
         const uint32_t bx0 = rx & 0xFFFFu, by0 = rx >> 16, w = (ry & 0xFFFFu) - bx0;
         for (uint32_t m = lane; m < sc; m += 32) {
-            const uint32_t key = (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
+            const uint32_t key = skb + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
             ekey[sb + m] = key;
             eval[sb + m] = sg;
             atomicAdd(&hist[key], 1u);
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+    for (int i = threadIdx.x; i < total_bins; i += blockDim.x)
         if (hist[i]) atomicAdd(&bin_count[i], hist[i]);
 }
 
-// Exclusive scan of the bin counts -> [begin, end) per bin (one CTA, nbins <= MAX_BINS).
-__global__ void __launch_bounds__(MAX_BINS) ranges_from_counts_kernel(const uint32_t* __restrict__ cnt, int nbins,
-                                                                      uint2* __restrict__ ranges) {
-    __shared__ uint32_t sc[MAX_BINS];
+// Exclusive scan of the bin counts -> [begin, end) per bin (one CTA of 1024 threads, two bins
+// per thread, nbins <= MAX_BINS = 2048).
+__global__ void __launch_bounds__(1024) ranges_from_counts_kernel(const uint32_t* __restrict__ cnt, int nbins,
+                                                                  uint2* __restrict__ ranges) {
+    __shared__ uint32_t sc[1024];
     const int t = threadIdx.x;
-    uint32_t c = t < nbins ? cnt[t] : 0u;
-    sc[t] = c;
+    const uint32_t c0 = 2 * t < nbins ? cnt[2 * t] : 0u, c1 = 2 * t + 1 < nbins ? cnt[2 * t + 1] : 0u;
+    sc[t] = c0 + c1;
     __syncthreads();
-    for (int o = 1; o < MAX_BINS; o <<= 1) {
+    for (int o = 1; o < 1024; o <<= 1) {
         uint32_t v = t >= o ? sc[t - o] : 0u;
         __syncthreads();
         sc[t] += v;
         __syncthreads();
     }
-    if (t < nbins) ranges[t] = make_uint2(sc[t] - c, sc[t]);
+    const uint32_t base = sc[t] - (c0 + c1);
+    if (2 * t < nbins) ranges[2 * t] = make_uint2(base, base + c0);
+    if (2 * t + 1 < nbins) ranges[2 * t + 1] = make_uint2(base + c0, base + c0 + c1);
 }
 
 // ------------------------------------------------------------------ ingest codes
@@ -411,27 +470,39 @@ void launch_activate(const float* means, const float* scales, const float* rots,
     activate_kernel<<<grid_for(G, 256), 256, 0, s>>>(means, scales, rots, opac, G, pg, err);
 }
 
-void launch_preprocess(PackedGaussians pg, int64_t G, Camera cam, Binning bn, ViewBuffers vb,
-                       unsigned long long* visible_ctr, cudaStream_t s) {
+void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s) {
     if (G <= 0) return;
-    preprocess_kernel<<<grid_for(G, 256), 256, 0, s>>>(pg, G, cam, bn, vb, visible_ctr);
+    const int64_t blocks = std::min<int64_t>((G + 255) / 256, 1184);
+    bounds_kernel<<<(unsigned)blocks, 256, 0, s>>>(pg, G, bbox);
 }
 
-void launch_gather_scan_input(const uint32_t* gidx_sorted, const uint32_t* tiles, uint64_t* out, int64_t G,
+void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
+                       int key_bits, unsigned long long* visible_ctr, ErrorLatch err, cudaStream_t s) {
+    if (G <= 0 || cams.n <= 0) return;
+    dim3 grid(grid_for(G, 256), (unsigned)cams.n);
+    preprocess_kernel<<<grid, 256, 0, s>>>(pg, G, cams, bn, vb, key_bits, visible_ctr, err);
+}
+
+void launch_gather_scan_input(const uint32_t* dval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
                               cudaStream_t s) {
-    if (G <= 0) return;
-    gather_tiles_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, tiles, out, G);
+    if (n <= 0) return;
+    gather_tiles_kernel<<<grid_for(n, 256), 256, 0, s>>>(dval_sorted, tiles, out, n);
 }
 
-void launch_emit(const uint32_t* gidx_sorted, const uint64_t* offsets, const uint2* rect, Binning bn, int64_t G,
-                 uint32_t* ekey, uint32_t* eval, uint32_t* bin_count, cudaStream_t s) {
-    if (G <= 0) return;
-    emit_kernel<<<grid_for(G, 256), 256, 0, s>>>(gidx_sorted, offsets, rect, bn.bins_x, bn.nbins(), G, ekey, eval,
-                                                 bin_count);
+void launch_view_totals(const uint64_t* offsets, int64_t G, int nviews, uint64_t* totals, cudaStream_t s) {
+    view_totals_kernel<<<1, 32, 0, s>>>(offsets, G, nviews, totals);
+}
+
+void launch_emit(const uint32_t* dval_sorted, const uint64_t* offsets, const uint2* rect, Binning bn, int64_t n,
+                 int64_t G, uint32_t* ekey, uint32_t* eval, uint32_t* bin_count, cudaStream_t s) {
+    if (n <= 0) return;
+    const int total_bins = (int)((n / G) * bn.nbins());
+    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(dval_sorted, offsets, rect, bn.bins_x, bn.nbins(), n, G, ekey, eval,
+                                                 bin_count, total_bins);
 }
 
 void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s) {
-    ranges_from_counts_kernel<<<1, MAX_BINS, 0, s>>>(bin_count, nbins, ranges);
+    ranges_from_counts_kernel<<<1, 1024, 0, s>>>(bin_count, nbins, ranges);
 }
 
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K, int L,

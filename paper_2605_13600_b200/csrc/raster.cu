@@ -54,7 +54,8 @@ __device__ __forceinline__ float exp2_spec(float y) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut) produce a
+// Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut; ext = support
+// box half-extents) produce a
 // fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r (square
 // support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative).  Margins make every
 // rounding here (and in the pixel's own fp32 evaluation of q, whose absolute error grows with
@@ -62,13 +63,13 @@ __device__ __forceinline__ float exp2_spec(float y) {
 // more: the rectangle is widened by 0.5 px and ycut relaxed by 0.01 + 2e-6 * (bound on the
 // terms of q over the rectangle).  Chords use the Schur form (peak of q along a line,
 // 4 qa qc - qb^2 in fp64) so elongated ellipses do not lose precision.
-__device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float X0, float X1, float Y0, float Y1) {
+__device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float2 ext, float X0, float X1, float Y0, float Y1) {
+    const float mx = a.x, my = a.y, r = a.z;
+    // support box of preprocess (square support intersected with the alpha >= 1/255 ellipse's
+    // box, padded by >= 1 px): pixel centres outside it never produce a fragment
+    if (mx + ext.x < X0 || mx - ext.x > X1 || my + ext.y < Y0 || my - ext.y > Y1) return false;
     const float M = 0.5f;
     X0 -= M; X1 += M; Y0 -= M; Y1 += M;
-    const float mx = a.x, my = a.y, r = a.z;
-    if (r < 0.f) return false;
-    // square support
-    if (mx + r < X0 || mx - r > X1 || my + r < Y0 || my - r > Y1) return false;
     // ellipse {q >= yc}: centre inside, or it meets an edge of the rectangle
     if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
     const float qa = b.x, qb = b.y, qc = b.z;
@@ -140,11 +141,14 @@ __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* a
     }
 }
 
+static_assert(BATCH == 32, "batch = one record per lane (transpose-reduction, flush indexing)");
+
 struct __align__(16) Smem {
     // ring of candidate records; slots [0, BATCH) are mirrored at [QCAP, QCAP + BATCH) so a
     // batch q_head .. q_head + BATCH - 1 is always contiguous
     float4 q0[QCAP + BATCH];   // (mx, my, r, o)
     float4 q1[QCAP + BATCH];   // (qa, qb, qc, ycut)
+    float2 q2[QCAP + BATCH];   // support-box half-extents
     uint32_t qg[QCAP + BATCH]; // Gaussian id
     float acc[2][MAX_SLOTS * BATCH];
     float accZ[2][BATCH];
@@ -163,15 +167,18 @@ struct __align__(16) Smem {
 #endif
 __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_kernel(const RasterParams p) {
     __shared__ Smem sm;
-    const int tile = blockIdx.x;
+    const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
+    const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
     const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
-    const uint2 range = p.ranges[bin];
+    const uint2 range = p.ranges[view * p.bn.nbins() + bin];
     if (range.x >= range.y) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wx0 = tx * TILE + 8 * (warp & 1), wy0 = ty * TILE + 4 * (warp >> 1);
     const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
-    const int Wd = p.cam.width, Hd = p.cam.height;
+    const int Wd = p.width, Hd = p.height;
+    const uint32_t jbase = (uint32_t)((int64_t)view * p.G);  // batch index of Gaussian 0 in this view
+    const int64_t code_row0 = p.code_row0[view];
     const bool inside = x < Wd && y < Hd;
     // pixel-centre rectangles of the tile and of this warp's 8x4 block (clipped to the image)
     const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
@@ -183,9 +190,9 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     // ---- setup: region key of my pixel, tile slot table, slot codes
     uint32_t key = KEY_NONE;
     if (inside) {
-        uint32_t rid = __ldg(p.region_ids + (int64_t)y * Wd + x);
-        if (rid != NONE && rid >= (uint32_t)p.num_regions) {
-            latch_error(p.err, ERR_REGION, p.pixel_base + (int64_t)y * Wd + x);
+        uint32_t rid = __ldg(p.region_ids[view] + (int64_t)y * Wd + x);
+        if (rid != NONE && rid >= (uint32_t)p.num_regions[view]) {
+            latch_error(p.err, ERR_REGION, p.pixel_base[view] + (int64_t)y * Wd + x);
             rid = NONE;
         }
         key = rid;
@@ -211,13 +218,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int nslot = sm.nslot;
     const bool overflow = sm.overflow != 0;
     const int S = p.S;
+    const int s_log2 = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
     for (int i = t; i < nslot * S; i += TILE_PIX) {
         const int q = i / S, s = i - q * S;
         const uint32_t k = sm.slot_key[q];
         uint32_t a = NONE;
         float c = 0.f;
         if (k != KEY_NONE) {
-            const int64_t row = (p.code_row0 + (int64_t)k) * S + s;
+            const int64_t row = (code_row0 + (int64_t)k) * S + s;
             a = __ldg(p.code_atoms + row);
             c = __ldg(p.code_coefs + row);
         }
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     }
     // (slot codes are first read after a later barrier)
     const bool coded = key != KEY_NONE;
-    const int64_t my_code_row = (p.code_row0 + (int64_t)(coded ? key : 0)) * S;
+    const int64_t my_code_row = (code_row0 + (int64_t)(coded ? key : 0)) * S;
 
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
     // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
@@ -247,11 +255,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             bool acc = false;
             uint32_t g = 0;
             float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+            float2 r2 = make_float2(-1.f, -1.f);
             if (idx < range.y) {
-                g = __ldg(p.eval + idx);
-                r0 = __ldg(p.rec0 + g);
-                r1 = __ldg(p.rec1 + g);
-                acc = rect_relevant(r0, r1, TX0, TX1, TY0, TY1);
+                const uint32_t jb = __ldg(p.eval + idx);  // batch index view*G + Gaussian
+                r0 = __ldg(p.rec0 + jb);
+                r1 = __ldg(p.rec1 + jb);
+                r2 = __ldg(p.rec2 + jb);
+                g = jb - jbase;
+                acc = rect_relevant(r0, r1, r2, TX0, TX1, TY0, TY1);
             }
             const unsigned bal = __ballot_sync(FULL, acc);
             if (lane == 0) sm.wcnt[warp] = __popc(bal);
@@ -268,10 +279,12 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 sm.qg[pos] = g;
                 sm.q0[pos] = r0;
                 sm.q1[pos] = r1;
+                sm.q2[pos] = r2;
                 if (pos < (uint32_t)BATCH) {
                     sm.qg[pos + QCAP] = g;
                     sm.q0[pos + QCAP] = r0;
                     sm.q1[pos + QCAP] = r1;
+                    sm.q2[pos + QCAP] = r2;
                 }
             }
             q_count += tot;
@@ -285,7 +298,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
         if (!warp_done && (uint32_t)lane < n) {
-            rel = rect_relevant(sm.q0[q_head + lane], sm.q1[q_head + lane], WX0, WX1, WY0, WY1);
+            rel = rect_relevant(sm.q0[q_head + lane], sm.q1[q_head + lane], sm.q2[q_head + lane], WX0, WX1, WY0, WY1);
         }
         const unsigned mask = __ballot_sync(FULL, rel);
 
@@ -360,9 +373,17 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             // ---- flush: S reds per (slot, Gaussian) into W, one per Gaussian into Z
             const int nitems = nslot * BATCH * S;
             for (int i = t; i < nitems; i += TILE_PIX) {
-                const int q = i / (BATCH * S);
-                const int rem = i - q * (BATCH * S);
-                const int j = rem / S, s = rem - j * S;
+                int q, j, s;
+                if (s_log2 >= 0) {  // S a power of two (every BASELINE config): shifts
+                    s = i & (S - 1);
+                    j = (i >> s_log2) & (BATCH - 1);
+                    q = i >> (s_log2 + 5);
+                } else {
+                    q = i / (BATCH * S);
+                    const int rem = i - q * (BATCH * S);
+                    j = rem / S;
+                    s = rem - j * S;
+                }
                 const float v = sm.acc[buf][q * BATCH + j];
                 const uint32_t a = sm.slot_atom[q][s];
                 if (v > 0.f && a != NONE)
@@ -392,7 +413,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     if (t == 0) {
         if (sm.contrib) {
             atomicAdd(p.contrib_ctr, sm.contrib);
-            if (p.contrib_out) atomicAdd(reinterpret_cast<unsigned long long*>(p.contrib_out), sm.contrib);
+            if (p.contrib_out[view]) atomicAdd(reinterpret_cast<unsigned long long*>(p.contrib_out[view]), sm.contrib);
         }
         if (sm.tests) atomicAdd(p.support_ctr, sm.tests);
     }
@@ -401,7 +422,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 }  // namespace
 
 void launch_raster(const RasterParams& p, cudaStream_t s) {
-    const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
+    const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (ntiles <= 0) return;
     static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the static 48 KB window");
     raster_aggregate_kernel<<<ntiles, TILE_PIX, 0, s>>>(p);
