@@ -18,6 +18,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,24 +94,36 @@ void grow(T** ptr, size_t* cap, size_t need, cudaStream_t s, double slack = 1.25
     *cap = n;
 }
 
-// One pipeline context: the buffers of one view batch and the stream it runs on.  Two
-// contexts alternate so that batch b+1's projection and depth sort overlap batch b's raster.
+// One pipeline context: the buffers of one view batch, the stream it runs on, and where the
+// batch is in its sequence of steps (DESIGN.md §5 a3).  Two contexts alternate, so that while
+// the host waits for one context's counts, the GPU runs the other context's queued work.
+enum Step : int { ST_IDLE = 0, ST_NEAR_FRONT, ST_NEAR_RASTER, ST_FAR_FRONT, ST_FAR_RASTER };
+
 struct Ctx {
     cudaStream_t s = nullptr;
-    cudaEvent_t ev_total = nullptr;
+    cudaEvent_t ev = nullptr;     // end of the last enqueued step (the host waits on it)
     ViewBuffers vb{};
-    size_t g_cap = 0, e_cap = 0, t_cap = 0;
+    size_t g_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_cap = 0;
-    uint64_t* h_total = nullptr;  // pinned [MAX_VB]: offsets at the end of each view
+    // pinned host staging
+    uint32_t* h_hist = nullptr;   // [MAX_VB * NHIST]
+    uint32_t* h_thr = nullptr;    // [MAX_VB]
+    uint64_t* h_total = nullptr;  // entries of the chunk
+    int* h_nsel = nullptr;        // selected elements of the far chunk
+    CamBatch* h_cams = nullptr;
     uint32_t* ids_stage = nullptr;
     size_t ids_cap = 0;
-    // launch state of the batch in flight (stage 1 done, stage 2 pending)
+    // the batch in flight
+    Step step = ST_IDLE;
     int v0 = 0, nv = 0;
-    int key_bits = 32;
+    int key_bits = 31;
+    int64_t nsel = 0;
+    bool far_any = false;
+    CamBatch cams{};
     const uint32_t* ids_dev[MAX_VB] = {};
-    // timing: ring of event sets (start/end of stage 1, binning start, raster start/end)
-    struct EvSet { cudaEvent_t e[5]; bool pending; int views; };
+    // timing: ring of event sets, 7 marks per batch (see ev_accumulate)
+    struct EvSet { cudaEvent_t e[7]; bool pending; int views; };
     std::vector<EvSet> evs;
     int ev_next = 0;
     int ev_cur = -1;
@@ -148,6 +161,7 @@ struct scoup_uplift {
     bool topk_pending = false;
     int64_t kernel_launches = 0, cub_launches = 0;
     double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
+    double near_frac = 0.1;             // near chunk: this fraction of each view's visible Gaussians
 };
 
 namespace {
@@ -171,43 +185,61 @@ scoup_status check_latched(scoup_uplift* h) {
 
 void ctx_init(Ctx& c) {
     CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&c.ev_total, cudaEventDisableTiming));
-    CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t) * MAX_VB));
+    CK(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
+    CK(cudaMallocHost((void**)&c.h_hist, sizeof(uint32_t) * MAX_VB * NHIST));
+    CK(cudaMallocHost((void**)&c.h_thr, sizeof(uint32_t) * MAX_VB));
+    CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t)));
+    CK(cudaMallocHost((void**)&c.h_nsel, sizeof(int)));
+    CK(cudaMallocHost((void**)&c.h_cams, sizeof(CamBatch)));
 }
 
 void ctx_free(Ctx& c, cudaStream_t s) {
     for (auto& es : c.evs)
-        for (int k = 0; k < 5; k++) cudaEventDestroy(es.e[k]);
+        for (int k = 0; k < 7; k++) cudaEventDestroy(es.e[k]);
     c.evs.clear();
     ViewBuffers& b = c.vb;
-    void* ptrs[] = {b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, b.tiles, b.offsets, b.rect,
-                    b.rec0, b.rec1, b.rec2, b.totals, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, b.bin_count,
-                    c.cub_tmp, c.ids_stage};
+    void* ptrs[] = {b.code, b.hist, b.thr, b.cams, b.sel, b.nsel, b.skey, b.skey_alt, b.sval, b.sval_sorted,
+                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.flags, b.live_sat, b.Tstate, b.tile_live, b.ekey, b.eval,
+                    b.ekey_alt, b.eval_alt, b.ranges, b.bin_count, c.cub_tmp, c.ids_stage};
     for (void* p : ptrs) dfree(p, s);
-    if (c.h_total) cudaFreeHost(c.h_total);
-    if (c.ev_total) cudaEventDestroy(c.ev_total);
+    void* hp[] = {c.h_hist, c.h_thr, c.h_total, c.h_nsel, c.h_cams};
+    for (void* p : hp)
+        if (p) cudaFreeHost(p);
+    if (c.ev) cudaEventDestroy(c.ev);
     if (c.s) cudaStreamDestroy(c.s);
     c = Ctx{};
 }
 
-// Per-(view, Gaussian) buffers for a batch of n = B*G elements.
-void ctx_reserve_gaussians(Ctx& c, int64_t n) {
-    if ((size_t)n <= c.g_cap && c.vb.depth_key) return;
+void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes, c.s); }
+
+// Per-(view, Gaussian) buffers for batches of up to n = B*G elements, per-pixel state for
+// B views of npx pixels, tile flags for B*ntiles tiles.
+void ctx_reserve(Ctx& c, int64_t n, int64_t pixels, int64_t tiles) {
     ViewBuffers& b = c.vb;
     n = std::max<int64_t>(n, 1);
-#define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
-    if (b.depth_key) {
-        void* ptrs[] = {b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, b.tiles, b.offsets, b.rect, b.rec0, b.rec1,
-                        b.rec2};
+    if ((size_t)n > c.g_cap || !b.code) {
+        void* ptrs[] = {b.code, b.sel, b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.offsets, b.rect,
+                        b.rec0, b.rec1, b.rec2, b.flags};
         for (void* p : ptrs) dfree(p, c.s);
-    }
-    RG(depth_key) RG(depth_key_alt) RG(dval) RG(dval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1) RG(rec2)
+#define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
+        RG(code) RG(sel) RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0)
+        RG(rec1) RG(rec2) RG(flags)
 #undef RG
-    if (!b.totals) dalloc(&b.totals, MAX_VB, c.s);
-    c.g_cap = (size_t)n;
+        c.g_cap = (size_t)n;
+    }
+    if (!b.hist) {
+        dalloc(&b.hist, (size_t)MAX_VB * NHIST, c.s);
+        dalloc(&b.thr, MAX_VB, c.s);
+        dalloc(&b.cams, 1, c.s);
+        dalloc(&b.nsel, 1, c.s);
+    }
+    grow(&b.Tstate, &c.px_cap, (size_t)std::max<int64_t>(pixels, 1), c.s, 1.0);
+    if ((size_t)std::max<int64_t>(tiles, 1) > c.tl_cap || !b.tile_live) {
+        dfree(b.live_sat, c.s);
+        dalloc(&b.live_sat, (size_t)MAX_VB * MAX_SAT_ENTRIES, c.s);
+    }
+    grow(&b.tile_live, &c.tl_cap, (size_t)std::max<int64_t>(tiles, 1), c.s, 1.0);
 }
-
-void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes, c.s); }
 
 bool rigid_ok(const float* M) {
     double R[3][3];
@@ -243,16 +275,16 @@ int bits_for(uint32_t n) {
 
 constexpr int EV_RING = 8;
 
+// Marks per batch: 0 start, 1 near front done, 2 near raster start, 3 near raster end,
+// 4 far front done, 5 far raster start, 6 far raster end.
 void ev_accumulate(scoup_uplift* h, Ctx::EvSet& es) {
     if (!es.pending) return;
-    CK(cudaEventSynchronize(es.e[4]));
-    float a = 0, b = 0, c = 0;
-    CK(cudaEventElapsedTime(&a, es.e[0], es.e[1]));
-    CK(cudaEventElapsedTime(&b, es.e[2], es.e[3]));
-    CK(cudaEventElapsedTime(&c, es.e[3], es.e[4]));
-    h->t_pre += a;
-    h->t_bin += b;
-    h->t_ras += c;
+    CK(cudaEventSynchronize(es.e[6]));
+    float t[6];
+    for (int k = 0; k < 6; k++) CK(cudaEventElapsedTime(&t[k], es.e[k], es.e[k + 1]));
+    h->t_pre += t[0] + t[3];
+    h->t_bin += t[1] + t[4];
+    h->t_ras += t[2] + t[5];
     h->ras_launches++;
     h->views_timed += es.views;
     es.pending = false;
@@ -263,7 +295,7 @@ Ctx::EvSet* ev_begin(scoup_uplift* h, Ctx& c) {
     if (c.evs.empty()) {
         c.evs.resize(EV_RING);
         for (auto& es : c.evs) {
-            for (int k = 0; k < 5; k++) CK(cudaEventCreate(&es.e[k]));
+            for (int k = 0; k < 7; k++) CK(cudaEventCreate(&es.e[k]));
             es.pending = false;
         }
     }
@@ -274,9 +306,10 @@ Ctx::EvSet* ev_begin(scoup_uplift* h, Ctx& c) {
     return &es;
 }
 
-Ctx::EvSet* ev_cur(Ctx& c) { return c.ev_cur >= 0 ? &c.evs[c.ev_cur] : nullptr; }
+void ev_mark(Ctx& c, int k) {
+    if (c.ev_cur >= 0) CK(cudaEventRecord(c.evs[c.ev_cur].e[k], c.s));
+}
 
-// Stage 1 of one view: preprocess, depth sort, scan -> total entries (async to pinned host).
 // Bin size: the smallest power-of-two group of tiles (>= 64x64 px) whose bin count fits one
 // 8-bit radix pass (<= 256 bins); very large images fall back to <= 1024 bins (2 passes).
 Binning choose_binning(int Wd, int Hd) {
@@ -327,51 +360,109 @@ int depth_key_bits(const scoup_uplift* h, const Camera* cams, int n) {
     return k;
 }
 
-// Stage 1 of a view batch: preprocess (all B views in one launch), one stable radix sort of
-// the (view, depth) keys, scan of the bin counts in that order -> per-view entry totals
-// (async to pinned host).
-void stage1(scoup_uplift* h, Ctx& c, const Camera* cams, int nv, const Binning& bn) {
-    const int64_t G = h->G;
-    const int64_t n = (int64_t)nv * G;
+// Per-call context of add_views shared by the steps.
+struct CallArgs {
+    const Camera* cams;
+    Binning bn;
+    const int64_t* code_row0;
+    const int32_t* num_regions;
+    int S;
+    long long* contrib_out;
+    int64_t npx;
+};
+
+// Depth pass of a batch: codes, per-view histogram (-> host), camera copy for the predicates.
+void step_depth(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     ViewBuffers& b = c.vb;
-    CamBatch cb{};
-    cb.n = nv;
-    for (int v = 0; v < nv; v++) cb.cam[v] = cams[v];
-    int vbits = 0;
-    while ((1 << vbits) < nv) vbits++;
-    const int kb = vbits == 0 ? 32 : c.key_bits;  // single view: full 32-bit code
-    const int end_bit = vbits == 0 ? 32 : kb + vbits;
     Ctx::EvSet* es = ev_begin(h, c);
-    if (es) { CK(cudaEventRecord(es->e[0], c.s)); es->views = nv; }
-    launch_preprocess(h->pg, G, cb, bn, b, kb, h->d_stats + 3, latch_of(h), c.s);
-    size_t need = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, (int)n, 0,
-                                       end_bit, c.s));
-    size_t need2 = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)n, c.s));
+    if (es) es->views = c.nv;
+    ev_mark(c, 0);
+    c.cams.n = c.nv;
+    for (int v = 0; v < c.nv; v++) c.cams.cam[v] = a.cams[c.v0 + v];
+    *c.h_cams = c.cams;
+    CK(cudaMemcpyAsync(b.cams, c.h_cams, sizeof(CamBatch), cudaMemcpyHostToDevice, c.s));
+    CK(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * NHIST * c.nv, c.s));
+    launch_depth_pass(h->pg, h->G, c.cams, c.key_bits, b.code, b.hist, h->d_stats + 3, latch_of(h), c.s);
+    CK(cudaMemcpyAsync(c.h_hist, b.hist, sizeof(uint32_t) * NHIST * c.nv, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev, c.s));
+    h->kernel_launches += 1;
+    c.step = ST_NEAR_FRONT;
+}
+
+// Front of one chunk on the nsel selected elements: EWA preprocess, depth sort, bin-count scan,
+// entry total -> host.
+void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
+    ViewBuffers& b = c.vb;
+    c.nsel = nsel;
+    if (nsel <= 0) return;
+    int vbits = 0;
+    while ((1 << vbits) < c.nv) vbits++;
+    const int end_bit = c.key_bits + vbits;
+    launch_preprocess(h->pg, h->G, c.cams, a.bn, b, c.key_bits, nsel, c.s);
+    size_t need = 0, need2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.skey, b.skey_alt, b.sval, b.sval_sorted, (int)nsel, 0, end_bit,
+                                       c.s));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)nsel, c.s));
     ctx_reserve_cub(c, std::max(need, need2));
-    CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.depth_key, b.depth_key_alt, b.dval, b.dval_sorted, (int)n,
-                                       0, end_bit, c.s));
-    launch_gather_scan_input(b.dval_sorted, b.tiles, b.offsets, n, c.s);
-    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)n, c.s));
-    launch_view_totals(b.offsets, G, nv, b.totals, c.s);
-    CK(cudaMemcpyAsync(c.h_total, b.totals, sizeof(uint64_t) * nv, cudaMemcpyDeviceToHost, c.s));
-    if (es) CK(cudaEventRecord(es->e[1], c.s));
-    CK(cudaEventRecord(c.ev_total, c.s));
-    h->kernel_launches += 3;
+    CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.skey, b.skey_alt, b.sval, b.sval_sorted, (int)nsel, 0,
+                                       end_bit, c.s));
+    launch_gather_scan_input(b.sval_sorted, b.tiles, b.offsets, nsel, c.s);
+    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)nsel, c.s));
+    CK(cudaMemcpyAsync(c.h_total, b.offsets + (nsel - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    h->kernel_launches += 2;
     h->cub_launches += 2;
 }
 
-// Stage 2 of a view batch: emit, bin sort, ranges, raster.  Needs stage 1's totals on the host.
-scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera* cams, const Binning& bn, const int64_t* code_row0,
-                    const int32_t* num_regions, int S, long long* contrib_out, int64_t npx) {
-    CK(cudaEventSynchronize(c.ev_total));
-    const int nv = c.nv;
-    const int64_t G = h->G;
-    const int64_t n = (int64_t)nv * G;
-    const uint64_t E = c.h_total[nv - 1];
-    const int nbins = bn.nbins() * nv;
+// Near chunk: per view, the nearest ~near_frac of the visible Gaussians (a histogram bucket
+// boundary of the depth code), stable-compacted, then the chunk front.
+void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
+    CK(cudaEventSynchronize(c.ev));
+    const uint32_t none = (1u << c.key_bits) - 1u;
+    const int shift = c.key_bits > HIST_BITS ? c.key_bits - HIST_BITS : 0;
+    int64_t n0 = 0;
+    c.far_any = false;
+    for (int v = 0; v < c.nv; v++) {
+        const uint32_t* hv = c.h_hist + (int64_t)v * NHIST;
+        uint64_t total = 0;
+        for (int k = 0; k < NHIST; k++) total += hv[k];
+        const uint64_t target = (uint64_t)std::ceil(h->near_frac * (double)total);
+        uint32_t thr = none;  // everything visible
+        uint64_t cum = 0;
+        if (target < total) {
+            for (int k = 0; k < NHIST; k++) {
+                cum += hv[k];
+                if (cum >= target) {
+                    thr = (uint32_t)std::min<uint64_t>((uint64_t)(k + 1) << shift, none);
+                    break;
+                }
+            }
+        } else {
+            cum = total;
+        }
+        if (cum < total) c.far_any = true;
+        c.h_thr[v] = thr;
+        n0 += (int64_t)cum;
+    }
     ViewBuffers& b = c.vb;
+    CK(cudaMemcpyAsync(b.thr, c.h_thr, sizeof(uint32_t) * c.nv, cudaMemcpyHostToDevice, c.s));
+    if (n0 > 0) {
+        const size_t need = select_temp_bytes((int64_t)c.nv * h->G);
+        ctx_reserve_cub(c, need);
+        launch_select_near(b, h->G, c.nv, c.key_bits, c.cub_tmp, c.cub_cap, c.s);
+        h->cub_launches += 1;
+    }
+    chunk_front(h, c, a, n0);
+    ev_mark(c, 1);
+    CK(cudaEventRecord(c.ev, c.s));
+    c.step = ST_NEAR_RASTER;
+}
+
+// Back of one chunk: emit, bin sort, ranges, raster.  Chunk 0 always launches the raster so
+// that every tile initialises its transmittance state.
+scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, int mark0) {
+    ViewBuffers& b = c.vb;
+    const uint64_t E = c.nsel > 0 ? *c.h_total : 0;
+    const int nbins = a.bn.nbins() * c.nv;
     if (E >= (uint64_t)INT32_MAX)
         return fail(SCOUP_EUNSUPPORTED, "view batch produces " + std::to_string(E) + " bin entries (>= 2^31)");
     if ((size_t)nbins > c.t_cap || !b.ranges) {
@@ -382,8 +473,11 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera* cams, const Binning& 
         c.t_cap = nbins;
     }
     h->host_entries += (int64_t)E;
-    Ctx::EvSet* es = ev_cur(c);
-    if (es) CK(cudaEventRecord(es->e[2], c.s));
+    if (E == 0 && chunk > 0) {
+        ev_mark(c, mark0);
+        ev_mark(c, mark0 + 1);
+        return SCOUP_OK;
+    }
     if (E > 0) {
         if (E > c.e_cap || !b.ekey) {
             size_t ne = (size_t)((double)E * 1.25);
@@ -396,54 +490,94 @@ scoup_status stage2(scoup_uplift* h, Ctx& c, const Camera* cams, const Binning& 
             c.e_cap = ne;
         }
         CK(cudaMemsetAsync(b.bin_count, 0, sizeof(uint32_t) * nbins, c.s));
-        launch_emit(b.dval_sorted, b.offsets, b.rect, bn, n, G, b.ekey, b.eval, b.bin_count, c.s);
+        int vbits = 0;
+        while ((1 << vbits) < c.nv) vbits++;
+        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b.rect, a.bn, c.nsel, c.nv,
+                    b.ekey, b.eval, b.bin_count, c.s);
         launch_ranges_from_counts(b.bin_count, nbins, b.ranges, c.s);
         const int nbits = bits_for((uint32_t)nbins);
         size_t need = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
         ctx_reserve_cub(c, need);
-        CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
-        RasterParams p{};
-        p.nviews = nv;
-        p.width = cams[0].width;
-        p.height = cams[0].height;
-        p.G = G;
-        p.bn = bn;
-        p.ranges = b.ranges;
-        p.eval = b.eval_alt;
-        p.rec0 = b.rec0;
-        p.rec1 = b.rec1;
-        p.rec2 = b.rec2;
-        for (int v = 0; v < nv; v++) {
-            const int u = c.v0 + v;
-            p.region_ids[v] = c.ids_dev[v];
-            p.code_row0[v] = code_row0[u];
-            p.num_regions[v] = num_regions[u];
-            p.pixel_base[v] = (long long)u * npx;
-            p.contrib_out[v] = contrib_out ? contrib_out + u : nullptr;
-        }
-        p.code_atoms = h->code_atoms;
-        p.code_coefs = h->code_coefs;
-        p.S = S;
-        p.L = h->L;
-        p.W = h->W;
-        p.Z = h->Z;
-        p.contrib_ctr = h->d_stats + 1;
-        p.support_ctr = h->d_stats + 4;
-        p.err = latch_of(h);
-        if (es) CK(cudaEventRecord(es->e[3], c.s));
-        launch_raster(p, c.s);
-        h->kernel_launches += 3;
+        CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits,
+                                           c.s));
+        h->kernel_launches += 2;
         h->cub_launches += 1;
-    } else if (es) {
-        CK(cudaEventRecord(es->e[3], c.s));
+    } else {
+        CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * nbins, c.s));
     }
-    if (es) {
-        CK(cudaEventRecord(es->e[4], c.s));
-        es->pending = true;
+    RasterParams p{};
+    p.nviews = c.nv;
+    p.width = a.cams[c.v0].width;
+    p.height = a.cams[c.v0].height;
+    p.G = h->G;
+    p.bn = a.bn;
+    p.ranges = b.ranges;
+    p.eval = b.eval_alt;
+    p.rec0 = b.rec0;
+    p.rec1 = b.rec1;
+    p.rec2 = b.rec2;
+    p.Tstate = b.Tstate;
+    p.tile_live = b.tile_live;
+    p.chunk = chunk;
+    for (int v = 0; v < c.nv; v++) {
+        const int u = c.v0 + v;
+        p.region_ids[v] = c.ids_dev[v];
+        p.code_row0[v] = a.code_row0[u];
+        p.num_regions[v] = a.num_regions[u];
+        p.pixel_base[v] = (long long)u * a.npx;
+        p.contrib_out[v] = a.contrib_out ? a.contrib_out + u : nullptr;
     }
-    CK(cudaGetLastError());
+    p.code_atoms = h->code_atoms;
+    p.code_coefs = h->code_coefs;
+    p.S = a.S;
+    p.L = h->L;
+    p.W = h->W;
+    p.Z = h->Z;
+    p.contrib_ctr = h->d_stats + 1;
+    p.support_ctr = h->d_stats + 4;
+    p.err = latch_of(h);
+    ev_mark(c, mark0);
+    launch_raster(p, c.s);
+    ev_mark(c, mark0 + 1);
+    h->kernel_launches += 1;
     return SCOUP_OK;
+}
+
+// Near raster, then the far selection: visible Gaussians beyond the split whose conservative
+// reach touches a tile that is still live (count -> host).
+scoup_status step_near_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
+    CK(cudaEventSynchronize(c.ev));
+    scoup_status st = chunk_back(h, c, a, 0, 2);
+    if (st != SCOUP_OK) return st;
+    if (c.far_any) {
+        const size_t need = select_temp_bytes((int64_t)c.nv * h->G);
+        ctx_reserve_cub(c, need);
+        launch_far_flags(c.vb, h->pg, h->G, c.cams, c.key_bits, a.bn, c.vb.flags, c.s);
+        launch_select_flagged(c.vb, c.vb.flags, (int64_t)c.nv * h->G, c.cub_tmp, c.cub_cap, c.s);
+        h->kernel_launches += 2;
+        CK(cudaMemcpyAsync(c.h_nsel, c.vb.nsel, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        h->cub_launches += 1;
+    }
+    CK(cudaEventRecord(c.ev, c.s));
+    c.step = ST_FAR_FRONT;
+    return SCOUP_OK;
+}
+
+void step_far_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
+    CK(cudaEventSynchronize(c.ev));
+    chunk_front(h, c, a, c.far_any ? (int64_t)*c.h_nsel : 0);
+    ev_mark(c, 4);
+    CK(cudaEventRecord(c.ev, c.s));
+    c.step = ST_FAR_RASTER;
+}
+
+scoup_status step_far_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
+    CK(cudaEventSynchronize(c.ev));
+    scoup_status st = chunk_back(h, c, a, 1, 5);
+    if (c.ev_cur >= 0) c.evs[c.ev_cur].pending = true;
+    c.step = ST_IDLE;
+    return st;
 }
 
 __global__ void add_u64(unsigned long long* p, unsigned long long v) { atomicAdd(p, v); }
@@ -516,6 +650,11 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
         dalloc(&h->pg.a, G, hs);
         dalloc(&h->pg.b, G, hs);
         dalloc(&h->pg.c, G, hs);
+        dalloc(&h->pg.s2, G, hs);
+        if (const char* nf = std::getenv("SCOUP_NEAR_FRAC")) {
+            const double f = std::atof(nf);
+            if (f > 0.0) h->near_frac = f;
+        }
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         for (int i = 0; i < 2; i++) {
             CK(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
@@ -598,6 +737,8 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
         rows = std::max<int64_t>(rows, code_row0[v] + num_regions[v]);
     }
     if ((int64_t)Wd * Hd >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "image too large");
+    if ((int64_t)((Wd + TILE - 1) / TILE + 1) * ((Hd + TILE - 1) / TILE + 1) > MAX_SAT_ENTRIES)
+        return fail(SCOUP_EUNSUPPORTED, "image too large for the tile tables (> 12288 16x16 tiles)");
     if (h->G == 0) return SCOUP_OK;
     const Binning bn = choose_binning(Wd, Hd);
     const int64_t npx = (int64_t)Wd * Hd;
@@ -630,40 +771,61 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             launch_ingest_codes(ain, cin, rows, S, h->K, h->L, h->code_atoms, h->code_coefs, latch_of(h), h->stream);
         }
         const bool ids_on_device = is_device_ptr(region_ids);
-        // ---- view batches: B views per pass (bounded by the bin-table size)
-        const int B = std::max(1, std::min(MAX_VB, std::min(MAX_BINS / bn.nbins(), (int)num_views)));
+        std::vector<Camera> cams(num_views);
+        for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
+        // ---- view batches: up to MAX_VB views per pass (bounded by the bin table and by the
+        // depth-code width: view bits + code bits <= 32)
+        const int Bmax = std::max(1, std::min(MAX_VB, std::min(MAX_BINS / bn.nbins(), (int)num_views)));
+        const int ntiles = bn.tiles_x * bn.tiles_y;
         // ---- fork the two pipeline contexts off the caller's stream
         CK(cudaEventRecord(h->ev_fork, h->stream));
         for (int i = 0; i < 2; i++) {
             CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
-            ctx_reserve_gaussians(h->ctx[i], (int64_t)B * h->G);
+            ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
         }
-        std::vector<Camera> cams(num_views);
-        for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
-        const int nbatch = (num_views + B - 1) / B;
-        scoup_status st = SCOUP_OK;
-        for (int bi = 0; bi <= nbatch && st == SCOUP_OK; bi++) {
-            if (bi < nbatch) {
-                Ctx& c = h->ctx[bi & 1];
-                c.v0 = bi * B;
-                c.nv = std::min(B, num_views - c.v0);
-                c.key_bits = depth_key_bits(h, &cams[c.v0], c.nv);
-                if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(B * npx), c.s, 1.0);
-                for (int v = 0; v < c.nv; v++) {
-                    const int u = c.v0 + v;
-                    if (ids_on_device) {
-                        c.ids_dev[v] = region_ids + (int64_t)u * npx;
-                    } else {
-                        CK(cudaMemcpyAsync(c.ids_stage + (int64_t)v * npx, region_ids + (int64_t)u * npx,
-                                           sizeof(uint32_t) * npx, cudaMemcpyHostToDevice, c.s));
-                        c.ids_dev[v] = c.ids_stage + (int64_t)v * npx;
-                    }
-                }
-                stage1(h, c, &cams[c.v0], c.nv, bn);
+        CallArgs args{cams.data(), bn, code_row0, num_regions, S, (long long*)contributions_out, npx};
+        int next = 0;  // first view not yet assigned to a batch
+        auto start_batch = [&](Ctx& c) {
+            int B = std::min(Bmax, num_views - next);
+            int kb = 31;
+            for (;; B = std::max(1, B / 2)) {
+                int vbits = 0;
+                while ((1 << vbits) < B) vbits++;
+                kb = std::min(31, depth_key_bits(h, &cams[next], B));
+                if (kb + vbits <= 32 || B == 1) break;
             }
-            if (bi > 0) {
-                Ctx& c = h->ctx[(bi - 1) & 1];
-                st = stage2(h, c, &cams[c.v0], bn, code_row0, num_regions, S, (long long*)contributions_out, npx);
+            c.v0 = next;
+            c.nv = B;
+            c.key_bits = kb;
+            next += B;
+            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx), c.s, 1.0);
+            for (int v = 0; v < c.nv; v++) {
+                const int u = c.v0 + v;
+                if (ids_on_device) {
+                    c.ids_dev[v] = region_ids + (int64_t)u * npx;
+                } else {
+                    CK(cudaMemcpyAsync(c.ids_stage + (int64_t)v * npx, region_ids + (int64_t)u * npx,
+                                       sizeof(uint32_t) * npx, cudaMemcpyHostToDevice, c.s));
+                    c.ids_dev[v] = c.ids_stage + (int64_t)v * npx;
+                }
+            }
+            step_depth(h, c, args);
+        };
+        scoup_status st = SCOUP_OK;
+        for (int ci = 0; ci < 2; ci++) h->ctx[ci].step = ST_IDLE;
+        for (bool busy = true; busy && st == SCOUP_OK;) {
+            busy = false;
+            for (int ci = 0; ci < 2 && st == SCOUP_OK; ci++) {
+                Ctx& c = h->ctx[ci];
+                switch (c.step) {
+                    case ST_IDLE:
+                        if (next < num_views) { start_batch(c); busy = true; }
+                        break;
+                    case ST_NEAR_FRONT: step_near_front(h, c, args); busy = true; break;
+                    case ST_NEAR_RASTER: st = step_near_raster(h, c, args); busy = true; break;
+                    case ST_FAR_FRONT: step_far_front(h, c, args); busy = true; break;
+                    case ST_FAR_RASTER: st = step_far_raster(h, c, args); busy = true; break;
+                }
             }
         }
         // ---- join back into the caller's stream
@@ -828,7 +990,7 @@ void scoup_uplift_free(scoup_uplift* h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     for (int i = 0; i < 2; i++)
         if (h->topk_ev[i]) cudaEventDestroy(h->topk_ev[i]);
-    void* ptrs[] = {h->pg.a, h->pg.b, h->pg.c, h->d_err_code, h->d_err_index, h->d_stats, h->code_atoms,
+    void* ptrs[] = {h->pg.a, h->pg.b, h->pg.c, h->pg.s2, h->d_err_code, h->d_err_index, h->d_stats, h->code_atoms,
                     h->code_coefs, h->code_atoms_in, h->code_coefs_in};
     for (void* p : ptrs) dfree(p, h->stream);
     if (h->own_wz) {

@@ -6,6 +6,9 @@
 //   ranges          per-tile [begin, end) of the tile-sorted entries
 //   ingest_codes    Algorithm 1's per-pixel TopK(W_v(p)) realised per region
 //   topk            Eq. 6 Top-K + L1 renormalisation (Algorithm 1)
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include <climits>
 
 #include <algorithm>
@@ -46,6 +49,7 @@ __global__ void activate_kernel(const float* __restrict__ means, const float* __
         pg.a[i] = make_float4(0.f, 0.f, 0.f, -1.f);
         pg.b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         pg.c[i] = make_float2(0.f, 0.f);
+        pg.s2[i] = 0.f;
         return;
     }
     float w = dv(qw, n), x = dv(qx, n), y = dv(qy, n), z = dv(qz, n);
@@ -75,6 +79,8 @@ __global__ void activate_kernel(const float* __restrict__ means, const float* __
     pg.a[i] = make_float4(mx, my, mz, o);
     pg.b[i] = make_float4(V[0], V[1], V[2], V[3]);
     pg.c[i] = make_float2(V[4], V[5]);
+    const float sm = fmaxf(s0, fmaxf(s1, s2));
+    pg.s2[i] = sm * sm * 1.0001f;  // lambda_max(Sigma_3D), padded (GPU-only prune)
 }
 
 // ------------------------------------------------------------------ scene bounds
@@ -107,31 +113,193 @@ __global__ void bounds_kernel(PackedGaussians pg, int64_t G, int* bbox) {
     }
 }
 
-// ------------------------------------------------------------------ preprocess (V1-V7)
-// One thread per (view, Gaussian): grid.y = view of the batch.  Writes the per-view records at
-// batch index j = v*G + i and the sort key (v << key_bits) | (bits(t_z) - bits(0.2f)), which
-// orders (view, depth) exactly (positive floats order as their bit patterns; the stable sort
-// keeps index order on ties); invisible Gaussians get the view's all-ones code.
-__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
-                                                         Binning bn, ViewBuffers vb, int key_bits,
-                                                         unsigned long long* visible_ctr, ErrorLatch err) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// ------------------------------------------------------------------ depth pass (V1, V2)
+// Depth code of a visible Gaussian: bits(t_z) - bits(0.2f) >= 1 (positive floats order as their
+// bit patterns, so codes order depths exactly; equal depths keep index order in the stable
+// sorts).  Invisible: the all-ones code `none`.
+__device__ __forceinline__ void camera_space(const float4& A, const Camera& cam, float t[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+        t[a] = add(add(add(mul(cam.P[4 * a + 0], A.x), mul(cam.P[4 * a + 1], A.y)), mul(cam.P[4 * a + 2], A.z)),
+                   cam.P[4 * a + 3]);
+}
+
+// Conservative screen-space reach of a Gaussian (GPU-only prune): with
+// lambda_max(Sigma_3D) = s_max^2 and ||J W||_2 <= ||J||_F, the square support r of V7 is at most
+// 3 sqrt(s_max^2 ||J||_F^2 + 0.3); padded for fp32 rounding.  mean2d is computed with the exact
+// V3 operations, so it equals preprocess's.
+__device__ __forceinline__ void reach(const float t[3], float s2max, const Camera& cam, float& mx, float& my,
+                                      float& rb) {
+    const float u = dv(t[0], t[2]), v = dv(t[1], t[2]);
+    mx = add(mul(cam.fx, u), cam.cx);
+    my = add(mul(cam.fy, v), cam.cy);
+    const float iz = 1.0f / t[2];
+    const float jf2 = (cam.fx * cam.fx * (1.0f + u * u) + cam.fy * cam.fy * (1.0f + v * v)) * iz * iz;
+    rb = 3.0f * sqrtf(s2max * jf2 + K_LOWPASS) * 1.002f + 1.0f;
+}
+
+__device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const Camera& cam) {
+    return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height &&
+           isfinite(mx) && isfinite(my) && isfinite(rb);
+}
+
+// One thread per (view, Gaussian), grid.y = view.  Writes code[j] (j = v*G + i) and the per-view
+// histogram of the codes' top HIST_BITS bits (near/far split, DESIGN.md §5 a3).  Off-screen
+// Gaussians (conservative reach misses the image) are invisible.
+// Each block covers ITEMS_PER_THREAD * 256 consecutive Gaussians of one view, so that the
+// shared histogram and the visible count are flushed to global memory once per block.
+constexpr int ITEMS_PER_THREAD = 16;
+
+__global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                         int key_bits, uint32_t* __restrict__ code,
+                                                         uint32_t* __restrict__ hist, unsigned long long* visible_ctr,
+                                                         ErrorLatch err) {
+    __shared__ uint32_t sh[NHIST];
+    __shared__ uint32_t svis;
+    for (int k = threadIdx.x; k < NHIST; k += blockDim.x) sh[k] = 0;
+    if (threadIdx.x == 0) svis = 0;
+    __syncthreads();
     const int view = blockIdx.y;
     const Camera& cam = cams.cam[view];
-    const int64_t j = (int64_t)view * G + i;
-    const uint32_t code_none = (key_bits >= 32) ? 0xFFFFFFFFu : ((1u << key_bits) - 1u);
-    bool vis = false;
-    if (i < G) {
-        float4 A = pg.a[i];
-        uint32_t key = code_none, ntiles = 0;
+    const uint32_t none = (1u << key_bits) - 1u;
+    const int shift = key_bits > HIST_BITS ? key_bits - HIST_BITS : 0;
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
+    uint32_t nvis = 0;
+    for (int it = 0; it < ITEMS_PER_THREAD; it++) {
+        const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
+        bool vis = false;
+        int bucket = -1;
+        if (i < G) {
+            const float4 A = pg.a[i];
+            uint32_t c = none;
+            float t[3];
+            camera_space(A, cam, t);
+            if (t[2] > K_NEAR && A.w >= K_AMIN) {
+                float mx, my, rb;
+                reach(t, pg.s2[i], cam, mx, my, rb);
+                if (box_on_image(mx, my, rb, cam)) {
+                    c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
+                    vis = c < none;
+                    if (!vis) {  // beyond the host's depth bound for the batch (cannot happen)
+                        latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + i);
+                        c = none;
+                    }
+                }
+            }
+            code[(int64_t)view * G + i] = c;
+            bucket = vis ? (int)(c >> shift) : -1;
+        }
+        // warp-aggregated histogram: one shared atomic per distinct bucket in the warp
+        const unsigned peers = __match_any_sync(0xffffffffu, bucket);
+        if (bucket >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bucket], (uint32_t)__popc(peers));
+        nvis += vis ? 1u : 0u;
+    }
+    nvis = __reduce_add_sync(0xffffffffu, nvis);
+    if ((threadIdx.x & 31) == 0 && nvis) atomicAdd(&svis, nvis);
+    __syncthreads();
+    for (int k = threadIdx.x; k < NHIST; k += blockDim.x)
+        if (sh[k]) atomicAdd(&hist[view * NHIST + k], sh[k]);
+    if (threadIdx.x == 0 && svis) atomicAdd(visible_ctr, (unsigned long long)svis);
+}
+
+// ------------------------------------------------------------------ chunk selection
+// Near chunk of view v: codes below thr[v].  Far chunk: the other visible codes whose
+// conservative reach touches a tile that is still live after the near chunk.  Both are stable
+// compactions (CUB DeviceSelect::If over the batch indices), so index order is kept.
+struct NearPred {
+    const uint32_t* code;
+    const uint32_t* thr;
+    int64_t G;
+    uint32_t none;
+    __device__ __forceinline__ bool operator()(uint32_t j) const {
+        const uint32_t c = code[j];
+        return c < thr[j / G] && c != none;
+    }
+};
+
+// Summed-area table of the live tiles of each view: sat[v][(ty+1)*(tx_n+1) + tx+1] = number of
+// live tiles in [0, tx] x [0, ty].  One block per view; rows then columns, in shared memory.
+
+__global__ void __launch_bounds__(1024) live_sat_kernel(const uint8_t* __restrict__ tile_live, int tiles_x,
+                                                        int tiles_y, uint32_t* __restrict__ sat) {
+    __shared__ uint32_t S[MAX_SAT_ENTRIES];
+    const int v = blockIdx.x;
+    const int W1 = tiles_x + 1, H1 = tiles_y + 1;
+    const uint8_t* lv = tile_live + (int64_t)v * tiles_x * tiles_y;
+    for (int k = threadIdx.x; k < W1 * H1; k += blockDim.x) {
+        const int x = k % W1, y = k / W1;
+        S[k] = (x > 0 && y > 0) ? (uint32_t)lv[(y - 1) * tiles_x + (x - 1)] : 0u;
+    }
+    __syncthreads();
+    for (int y = threadIdx.x; y < H1; y += blockDim.x)
+        for (int x = 1; x < W1; x++) S[y * W1 + x] += S[y * W1 + x - 1];
+    __syncthreads();
+    for (int x = threadIdx.x; x < W1; x += blockDim.x)
+        for (int y = 1; y < H1; y++) S[y * W1 + x] += S[(y - 1) * W1 + x];
+    __syncthreads();
+    for (int k = threadIdx.x; k < W1 * H1; k += blockDim.x) sat[(int64_t)v * W1 * H1 + k] = S[k];
+}
+
+// Far flags: one thread per (view, Gaussian) of the far range; kept when its conservative reach
+// box covers a live tile (a fragment needs |x + 0.5 - mean.x| <= r <= rb, same in y), which the
+// summed-area table answers in four loads.
+__global__ void __launch_bounds__(256) far_flags_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                        const uint32_t* __restrict__ code,
+                                                        const uint32_t* __restrict__ thr, uint32_t none,
+                                                        const uint32_t* __restrict__ sat, int tiles_x,
+                                                        int tiles_y, uint8_t* __restrict__ flags) {
+    const int view = blockIdx.y;
+    const int W1 = tiles_x + 1;
+    const uint32_t* S = sat + (int64_t)view * W1 * (tiles_y + 1);
+    const Camera& cam = cams.cam[view];
+    const uint32_t tv = thr[view];
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
+    for (int it = 0; it < ITEMS_PER_THREAD; it++) {
+        const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
+        if (i >= G) break;
+        const int64_t j = (int64_t)view * G + i;
+        const uint32_t c = code[j];
+        bool keep = false;
+        if (c != none && c >= tv) {
+            float t[3];
+            camera_space(pg.a[i], cam, t);
+            float mx, my, rb;
+            reach(t, pg.s2[i], cam, mx, my, rb);
+            // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
+            const int x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
+            const int x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
+            const int y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
+            const int y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+            if (x0 <= x1 && y0 <= y1) {
+                const uint32_t n = __ldg(S + (y1 + 1) * W1 + x1 + 1) - __ldg(S + y0 * W1 + x1 + 1) -
+                                   __ldg(S + (y1 + 1) * W1 + x0) + __ldg(S + y0 * W1 + x0);
+                keep = n > 0;
+            }
+        }
+        flags[j] = keep ? 1 : 0;
+    }
+}
+
+// ------------------------------------------------------------------ preprocess (V2-V7)
+// One thread per selected element e (batch index j = sel[e], view v = j / G, Gaussian i): the EWA
+// records at e (compact), the bin count of the support rectangle, and the sort pair
+// ((v << key_bits) | code, e).
+__global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                         Binning bn, ViewBuffers vb, int key_bits,
+                                                         const uint32_t* __restrict__ sel, int64_t nsel,
+                                                         uint32_t* __restrict__ skey, uint32_t* __restrict__ sval) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nsel) return;
+    const uint32_t j = sel[e];
+    const int view = (int)(j / G);
+    const int64_t i = (int64_t)j - (int64_t)view * G;
+    const Camera& cam = cams.cam[view];
+    {
+        const float4 A = pg.a[i];
+        uint32_t ntiles = 0;
         const float o = A.w;
-        // V1: camera-space mean
         float t[3];
-#pragma unroll
-        for (int a = 0; a < 3; a++)
-            t[a] = add(add(add(mul(cam.P[4 * a + 0], A.x), mul(cam.P[4 * a + 1], A.y)),
-                           mul(cam.P[4 * a + 2], A.z)),
-                       cam.P[4 * a + 3]);
+        camera_space(A, cam, t);
         // V2: near plane; exact opacity cull (alpha <= o < 1/255 never contributes)
         if (t[2] > K_NEAR && o >= K_AMIN) {
             float4 B = pg.b[i];
@@ -212,49 +380,36 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                     int y0 = (int)fmaxf(fy0, 0.f), y1 = (int)fminf(fy1, Hm1);
                     int tx0 = x0 >> bn.bshx, tx1 = (x1 >> bn.bshx) + 1, ty0 = y0 >> bn.bshy, ty1 = (y1 >> bn.bshy) + 1;
                     ntiles = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
-                    key = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);  // >= 1 (t_z > 0.2f)
-                    if (key >= code_none) {  // beyond the host's depth bound (cannot happen)
-                        latch_error(err, ERR_DEPTHKEY, j);
-                        key = code_none - 1u;
-                    }
-                    vb.rect[j] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
-                    vb.rec0[j] = make_float4(mx, my, r, o);
-                    vb.rec1[j] = make_float4(qa, qb, qc, ycut);
-                    vb.rec2[j] = make_float2(hx + padx, hy + pady);
-                    vis = true;
+                    vb.rect[e] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
+                    vb.rec0[e] = make_float4(mx, my, r, o);
+                    vb.rec1[e] = make_float4(qa, qb, qc, ycut);
+                    vb.rec2[e] = make_float4(hx + padx, hy + pady, __uint_as_float((uint32_t)i), 0.f);
                 }
             }
         }
-        vb.depth_key[j] = key_bits >= 32 ? key : (((uint32_t)view << key_bits) | key);
-        vb.tiles[j] = ntiles;
-        vb.dval[j] = (uint32_t)j;
+        vb.tiles[e] = ntiles;
+        skey[e] = ((uint32_t)view << key_bits) | vb.code[j];
+        sval[e] = (uint32_t)e;
     }
-    unsigned ballot = __ballot_sync(0xffffffffu, vis);
-    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(visible_ctr, (unsigned long long)__popc(ballot));
 }
 
-__global__ void gather_tiles_kernel(const uint32_t* __restrict__ dval_sorted, const uint32_t* __restrict__ tiles,
+__global__ void gather_tiles_kernel(const uint32_t* __restrict__ sval_sorted, const uint32_t* __restrict__ tiles,
                                     uint64_t* __restrict__ out, int64_t n) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) out[k] = tiles[dval_sorted[k]];
-}
-
-// totals[v] = inclusive offset at the end of view v's sorted segment [v*G, (v+1)*G)
-__global__ void view_totals_kernel(const uint64_t* __restrict__ offsets, int64_t G, int nviews,
-                                   uint64_t* __restrict__ totals) {
-    const int v = threadIdx.x;
-    if (v < nviews) totals[v] = G > 0 ? offsets[(int64_t)(v + 1) * G - 1] : 0ull;
+    if (k < n) out[k] = tiles[sval_sorted[k]];
 }
 
 // ------------------------------------------------------------------ emit
-// Entry m of the element at sorted position k (view v = k / G) goes to slot offsets[k-1] + m
+// Entry m of the element at sorted position k (chunk index e, view v = sorted key >> key_bits) goes
+// to slot offsets[k-1] + m
 // with key v*nbins + bin, so the entries are in (view, depth, index) order before the stable
 // bin sort.  Per-bin entry counts are accumulated through a shared-memory histogram (they give
 // the bin ranges directly).
-__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ dval_sorted,
+__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ sval_sorted,
+                                                   const uint32_t* __restrict__ skey_sorted, int key_bits,
                                                    const uint64_t* __restrict__ offsets,
                                                    const uint2* __restrict__ rect, int bins_x, int nbins, int64_t n,
-                                                   int64_t G, uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
+                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
                                                    uint32_t* __restrict__ bin_count, int total_bins) {
     __shared__ uint32_t hist[MAX_BINS];
     for (int i = threadIdx.x; i < total_bins; i += blockDim.x) hist[i] = 0;
@@ -268,9 +423,9 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
         begin = k > 0 ? offsets[k - 1] : 0;
         end = offsets[k];
         if (end > begin) {
-            g = dval_sorted[k];
+            g = sval_sorted[k];
             rc = rect[g];
-            kbase = (uint32_t)(k / G) * (uint32_t)nbins;
+            kbase = (key_bits >= 32 ? 0u : (skey_sorted[k] >> key_bits)) * (uint32_t)nbins;
         }
     }
     const uint32_t cnt = (uint32_t)(end - begin);
@@ -476,29 +631,64 @@ void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s) {
     bounds_kernel<<<(unsigned)blocks, 256, 0, s>>>(pg, G, bbox);
 }
 
-void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
-                       int key_bits, unsigned long long* visible_ctr, ErrorLatch err, cudaStream_t s) {
+void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* code,
+                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, cudaStream_t s) {
     if (G <= 0 || cams.n <= 0) return;
-    dim3 grid(grid_for(G, 256), (unsigned)cams.n);
-    preprocess_kernel<<<grid, 256, 0, s>>>(pg, G, cams, bn, vb, key_bits, visible_ctr, err);
+    dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
+    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, code, hist, visible_ctr, err);
 }
 
-void launch_gather_scan_input(const uint32_t* dval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
+size_t select_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    thrust::counting_iterator<uint32_t> it(0);
+    NearPred np{};
+    cub::DeviceSelect::If(nullptr, a, it, (uint32_t*)nullptr, (int*)nullptr, (int)n, np);
+    cub::DeviceSelect::Flagged(nullptr, b, it, (const uint8_t*)nullptr, (uint32_t*)nullptr, (int*)nullptr, (int)n);
+    return std::max(a, b);
+}
+
+void launch_select_near(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, void* tmp, size_t tmp_bytes,
+                        cudaStream_t s) {
+    const int64_t n = (int64_t)nviews * G;
+    NearPred pred{vb.code, vb.thr, G, (1u << key_bits) - 1u};
+    cub::DeviceSelect::If(tmp, tmp_bytes, thrust::counting_iterator<uint32_t>(0), vb.sel, vb.nsel, (int)n, pred, s);
+}
+
+void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
+                      const Binning& bn, uint8_t* flags, cudaStream_t s) {
+    if (G <= 0 || cams.n <= 0) return;
+    live_sat_kernel<<<cams.n, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, vb.live_sat);
+    dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
+    far_flags_kernel<<<grid, 256, 0, s>>>(pg, G, cams, vb.code, vb.thr, (1u << key_bits) - 1u, vb.live_sat,
+                                          bn.tiles_x, bn.tiles_y, flags);
+}
+
+void launch_select_flagged(const ViewBuffers& vb, const uint8_t* flags, int64_t n, void* tmp, size_t tmp_bytes,
+                           cudaStream_t s) {
+    cub::DeviceSelect::Flagged(tmp, tmp_bytes, thrust::counting_iterator<uint32_t>(0), flags, vb.sel, vb.nsel, (int)n,
+                               s);
+}
+
+void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
+                       int key_bits, int64_t nsel, cudaStream_t s) {
+    if (nsel <= 0) return;
+    preprocess_kernel<<<grid_for(nsel, 256), 256, 0, s>>>(pg, G, cams, bn, vb, key_bits, vb.sel, nsel, vb.skey,
+                                                          vb.sval);
+}
+
+void launch_gather_scan_input(const uint32_t* sval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
                               cudaStream_t s) {
     if (n <= 0) return;
-    gather_tiles_kernel<<<grid_for(n, 256), 256, 0, s>>>(dval_sorted, tiles, out, n);
+    gather_tiles_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, tiles, out, n);
 }
 
-void launch_view_totals(const uint64_t* offsets, int64_t G, int nviews, uint64_t* totals, cudaStream_t s) {
-    view_totals_kernel<<<1, 32, 0, s>>>(offsets, G, nviews, totals);
-}
-
-void launch_emit(const uint32_t* dval_sorted, const uint64_t* offsets, const uint2* rect, Binning bn, int64_t n,
-                 int64_t G, uint32_t* ekey, uint32_t* eval, uint32_t* bin_count, cudaStream_t s) {
+void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int key_bits, const uint64_t* offsets,
+                 const uint2* rect, Binning bn, int64_t n, int nviews, uint32_t* ekey, uint32_t* eval,
+                 uint32_t* bin_count, cudaStream_t s) {
     if (n <= 0) return;
-    const int total_bins = (int)((n / G) * bn.nbins());
-    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(dval_sorted, offsets, rect, bn.bins_x, bn.nbins(), n, G, ekey, eval,
-                                                 bin_count, total_bins);
+    const int total_bins = nviews * bn.nbins();
+    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, skey_sorted, key_bits, offsets, rect, bn.bins_x,
+                                                 bn.nbins(), n, ekey, eval, bin_count, total_bins);
 }
 
 void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s) {

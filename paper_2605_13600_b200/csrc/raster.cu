@@ -171,15 +171,23 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
     const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
+    const int64_t gtile = (int64_t)view * ntiles + tile;
+    if (p.chunk > 0 && !p.tile_live[gtile]) return;  // every pixel finished in an earlier chunk
     const uint2 range = p.ranges[view * p.bn.nbins() + bin];
-    if (range.x >= range.y) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wx0 = tx * TILE + 8 * (warp & 1), wy0 = ty * TILE + 4 * (warp >> 1);
     const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
     const int Wd = p.width, Hd = p.height;
-    const uint32_t jbase = (uint32_t)((int64_t)view * p.G);  // batch index of Gaussian 0 in this view
-    const int64_t code_row0 = p.code_row0[view];
     const bool inside = x < Wd && y < Hd;
+    float* Tpix = p.Tstate + (int64_t)view * Wd * Hd + (int64_t)y * Wd + x;
+    if (range.x >= range.y) {  // nothing of this chunk reaches the tile
+        if (p.chunk == 0) {
+            if (inside) *Tpix = 1.0f;
+            if (t == 0) p.tile_live[gtile] = 1;
+        }
+        return;
+    }
+    const int64_t code_row0 = p.code_row0[view];
     // pixel-centre rectangles of the tile and of this warp's 8x4 block (clipped to the image)
     const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
     const float TX1 = (float)(min(tx * TILE + TILE, Wd) - 1) + 0.5f;
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
     // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
     // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
-    float T = inside ? 1.0f : 0.0f;
+    float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
     uint32_t cnt = 0, tests = 0;
     float* Wm = p.W;
     const int L = p.L;
@@ -257,11 +265,12 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
             float2 r2 = make_float2(-1.f, -1.f);
             if (idx < range.y) {
-                const uint32_t jb = __ldg(p.eval + idx);  // batch index view*G + Gaussian
-                r0 = __ldg(p.rec0 + jb);
-                r1 = __ldg(p.rec1 + jb);
-                r2 = __ldg(p.rec2 + jb);
-                g = jb - jbase;
+                const uint32_t e = __ldg(p.eval + idx);  // chunk index of the Gaussian
+                r0 = __ldg(p.rec0 + e);
+                r1 = __ldg(p.rec1 + e);
+                const float4 r2e = __ldg(p.rec2 + e);
+                r2 = make_float2(r2e.x, r2e.y);
+                g = __float_as_uint(r2e.z);
                 acc = rect_relevant(r0, r1, r2, TX0, TX1, TY0, TY1);
             }
             const unsigned bal = __ballot_sync(FULL, acc);
@@ -403,6 +412,11 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         buf ^= 1;
         if (__syncthreads_count(T > 0.f) == 0) break;  // B2
     }
+
+    // carry the per-pixel state to the next chunk
+    if (inside) *Tpix = T;
+    const int live = __syncthreads_count(T > 0.f);
+    if (t == 0) p.tile_live[gtile] = live > 0 ? 1 : 0;
 
     // contributions (terms of Eq. 5's sum) and support tests
     const unsigned c = __reduce_add_sync(FULL, cnt);
