@@ -115,6 +115,17 @@ def measured_peaks():
         return {}
 
 
+def measured_traffic():
+    """DRAM bytes of the fused kernel from the committed ncu capture (profiles/raster_traffic.json),
+    per view (a launch covers a batch of views), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "raster_traffic.json")) as fh:
+            t = json.load(fh)
+        return (t["dram_bytes_read"] + t["dram_bytes_write"]) / t["views_per_launch"], t["source"]
+    except Exception:
+        return None, None
+
+
 def crop_band(cam, y0, y1):
     """The rows [y0, y1) of a view as a camera of its own (same rays; principal point shifted)."""
     from paper_2605_13600_b200 import synth
@@ -273,6 +284,7 @@ def main():
     ops_step = OPS_PER_TEST * st["support_tests"] + (2 * cfg.S + 1) * st["contributions"]
     ras_step_s = tm["raster_ms"] / args.steps / 1e3
     achieved = ops_step / ras_step_s / 1e12 if ras_step_s > 0 else 0.0
+    traffic_view, traffic_src = measured_traffic()
     total_dev_ms = tm["preprocess_ms"] + tm["binning_ms"] + tm["raster_ms"] + tm["topk_ms"]
 
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
@@ -336,7 +348,8 @@ def main():
             "device_ms_per_step": {k: tm[k] / args.steps for k in ("preprocess_ms", "binning_ms", "raster_ms", "topk_ms")},
             "roofline": {"bound": "alu", "kernel": "raster_aggregate_kernel", "achieved": achieved,
                          "peak": alu_peak, "unit": "T lane-ops/s", "frac": achieved / alu_peak,
-                         "traffic": None, "avg_launch_ms": ras_avg_s * 1e3,
+                         "traffic": traffic_view, "traffic_unit": "DRAM bytes per view (ncu)",
+                         "traffic_source": traffic_src, "avg_launch_ms": ras_avg_s * 1e3,
                          "views_per_launch": tm["views_timed"] / launches,
                          "share_of_step": tm["raster_ms"] / max(1e-9, total_dev_ms),
                          "peak_source": f"{sms} SMs x 128 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
