@@ -162,6 +162,7 @@ struct scoup_uplift {
     int64_t kernel_launches = 0, cub_launches = 0;
     double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
     double near_frac = 0.1;             // near chunk: this fraction of each view's visible Gaussians
+    int bin_shift = 6;                  // bins of 2^bin_shift px squares
 };
 
 namespace {
@@ -199,8 +200,8 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     c.evs.clear();
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.code, b.hist, b.thr, b.cams, b.sel, b.nsel, b.skey, b.skey_alt, b.sval, b.sval_sorted,
-                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.flags, b.live_sat, b.Tstate, b.tile_live, b.ekey, b.eval,
-                    b.ekey_alt, b.eval_alt, b.ranges, b.bin_count, c.cub_tmp, c.ids_stage};
+                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.flags, b.live_sat, b.Tstate, b.tile_live, b.ekey, b.eval,
+                    b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp, c.ids_stage};
     for (void* p : ptrs) dfree(p, s);
     void* hp[] = {c.h_hist, c.h_thr, c.h_total, c.h_nsel, c.h_cams};
     for (void* p : hp)
@@ -219,11 +220,11 @@ void ctx_reserve(Ctx& c, int64_t n, int64_t pixels, int64_t tiles) {
     n = std::max<int64_t>(n, 1);
     if ((size_t)n > c.g_cap || !b.code) {
         void* ptrs[] = {b.code, b.sel, b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.offsets, b.rect,
-                        b.rec0, b.rec1, b.rec2, b.flags};
+                        b.rec0, b.rec1, b.rec2, b.rec3, b.flags};
         for (void* p : ptrs) dfree(p, c.s);
 #define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
         RG(code) RG(sel) RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0)
-        RG(rec1) RG(rec2) RG(flags)
+        RG(rec1) RG(rec2) RG(rec3) RG(flags)
 #undef RG
         c.g_cap = (size_t)n;
     }
@@ -310,26 +311,15 @@ void ev_mark(Ctx& c, int k) {
     if (c.ev_cur >= 0) CK(cudaEventRecord(c.evs[c.ev_cur].e[k], c.s));
 }
 
-// Bin size: the smallest power-of-two group of tiles (>= 64x64 px) whose bin count fits one
-// 8-bit radix pass (<= 256 bins); very large images fall back to <= 1024 bins (2 passes).
-Binning choose_binning(int Wd, int Hd) {
+// Bins: squares of 2^bin_shift px (default 64x64, SCOUP_BIN_SHIFT) holding the depth-ordered
+// candidates of the 16x16 tiles inside them; each tile filters its bin's list (band_relevant).
+Binning choose_binning(int Wd, int Hd, int bin_shift) {
     Binning b;
     b.tiles_x = (Wd + TILE - 1) / TILE;
     b.tiles_y = (Hd + TILE - 1) / TILE;
-    const int cand[][2] = {{6, 6}, {7, 6}, {7, 7}, {8, 7}, {8, 8}, {9, 8}, {9, 9}, {10, 9}, {10, 10}, {11, 10},
-                           {11, 11}, {12, 11}, {12, 12}};
-    for (int lim : {256, 1024}) {
-        for (auto& c : cand) {
-            int bx = (Wd + (1 << c[0]) - 1) >> c[0], by = (Hd + (1 << c[1]) - 1) >> c[1];
-            if (bx * by <= lim) {
-                b.bshx = c[0]; b.bshy = c[1]; b.bins_x = bx; b.bins_y = by;
-                return b;
-            }
-        }
-    }
-    b.bshx = b.bshy = 12;
-    b.bins_x = (Wd + 4095) >> 12;
-    b.bins_y = (Hd + 4095) >> 12;
+    b.bshx = b.bshy = bin_shift;
+    b.bins_x = (Wd + (1 << bin_shift) - 1) >> bin_shift;
+    b.bins_y = (Hd + (1 << bin_shift) - 1) >> bin_shift;
     return b;
 }
 
@@ -457,20 +447,18 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     c.step = ST_NEAR_RASTER;
 }
 
-// Back of one chunk: emit, bin sort, ranges, raster.  Chunk 0 always launches the raster so
-// that every tile initialises its transmittance state.
+// Back of one chunk: emit (tile-exact), tile sort, ranges, raster.  Chunk 0 always launches the
+// raster so that every tile initialises its transmittance state.
 scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, int mark0) {
     ViewBuffers& b = c.vb;
     const uint64_t E = c.nsel > 0 ? *c.h_total : 0;
-    const int nbins = a.bn.nbins() * c.nv;
+    const int ntiles = a.bn.nbins() * c.nv;  // bins of the batch (= the ranges' sentinel key)
     if (E >= (uint64_t)INT32_MAX)
-        return fail(SCOUP_EUNSUPPORTED, "view batch produces " + std::to_string(E) + " bin entries (>= 2^31)");
-    if ((size_t)nbins > c.t_cap || !b.ranges) {
+        return fail(SCOUP_EUNSUPPORTED, "view batch produces " + std::to_string(E) + " tile entries (>= 2^31)");
+    if ((size_t)ntiles > c.t_cap || !b.ranges) {
         dfree(b.ranges, c.s);
-        dfree(b.bin_count, c.s);
-        dalloc(&b.ranges, nbins, c.s);
-        dalloc(&b.bin_count, nbins, c.s);
-        c.t_cap = nbins;
+        dalloc(&b.ranges, ntiles, c.s);
+        c.t_cap = ntiles;
     }
     h->host_entries += (int64_t)E;
     if (E == 0 && chunk > 0) {
@@ -478,6 +466,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
         ev_mark(c, mark0 + 1);
         return SCOUP_OK;
     }
+    CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * ntiles, c.s));
     if (E > 0) {
         if (E > c.e_cap || !b.ekey) {
             size_t ne = (size_t)((double)E * 1.25);
@@ -489,22 +478,19 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
             dalloc(&b.eval_alt, ne, c.s);
             c.e_cap = ne;
         }
-        CK(cudaMemsetAsync(b.bin_count, 0, sizeof(uint32_t) * nbins, c.s));
         int vbits = 0;
         while ((1 << vbits) < c.nv) vbits++;
-        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b.rect, a.bn, c.nsel, c.nv,
-                    b.ekey, b.eval, b.bin_count, c.s);
-        launch_ranges_from_counts(b.bin_count, nbins, b.ranges, c.s);
-        const int nbits = bits_for((uint32_t)nbins);
+        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b, a.bn, a.cams[c.v0].width,
+                    a.cams[c.v0].height, c.nsel, c.nv, b.ekey, b.eval, c.s);
+        const int nbits = bits_for((uint32_t)ntiles + 1u);
         size_t need = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
         ctx_reserve_cub(c, need);
         CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits,
                                            c.s));
+        launch_ranges(b.ekey_alt, (int64_t)E, (uint32_t)ntiles, b.ranges, c.s);
         h->kernel_launches += 2;
         h->cub_launches += 1;
-    } else {
-        CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * nbins, c.s));
     }
     RasterParams p{};
     p.nviews = c.nv;
@@ -517,6 +503,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.rec0 = b.rec0;
     p.rec1 = b.rec1;
     p.rec2 = b.rec2;
+    p.rec3 = b.rec3;
     p.Tstate = b.Tstate;
     p.tile_live = b.tile_live;
     p.chunk = chunk;
@@ -655,6 +642,10 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
             const double f = std::atof(nf);
             if (f > 0.0) h->near_frac = f;
         }
+        if (const char* bs = std::getenv("SCOUP_BIN_SHIFT")) {
+            const int v = std::atoi(bs);
+            if (v >= 4 && v <= 10) h->bin_shift = v;
+        }
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         for (int i = 0; i < 2; i++) {
             CK(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
@@ -740,7 +731,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
     if ((int64_t)((Wd + TILE - 1) / TILE + 1) * ((Hd + TILE - 1) / TILE + 1) > MAX_SAT_ENTRIES)
         return fail(SCOUP_EUNSUPPORTED, "image too large for the tile tables (> 12288 16x16 tiles)");
     if (h->G == 0) return SCOUP_OK;
-    const Binning bn = choose_binning(Wd, Hd);
+    const Binning bn = choose_binning(Wd, Hd, h->bin_shift);
     const int64_t npx = (int64_t)Wd * Hd;
     try {
         DeviceGuard dg(h->device);
@@ -775,7 +766,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
         for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
         // ---- view batches: up to MAX_VB views per pass (bounded by the bin table and by the
         // depth-code width: view bits + code bits <= 32)
-        const int Bmax = std::max(1, std::min(MAX_VB, std::min(MAX_BINS / bn.nbins(), (int)num_views)));
+        const int Bmax = std::max(1, std::min(MAX_VB, (int)num_views));
         const int ntiles = bn.tiles_x * bn.tiles_y;
         // ---- fork the two pipeline contexts off the caller's stream
         CK(cudaEventRecord(h->ev_fork, h->stream));

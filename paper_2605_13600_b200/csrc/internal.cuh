@@ -17,7 +17,6 @@ constexpr int BATCH = 32;                // Gaussians staged per raster batch
 constexpr int MAX_SLOTS = 32;            // distinct regions per tile on the smem-aggregated path
 constexpr int MAX_S = 16;
 constexpr int MAX_VB = 8;                // views batched per preprocess/sort/raster pass
-constexpr int MAX_BINS = 2048;           // bins per view batch (views x bins per view)
 constexpr int MAX_SAT_ENTRIES = 12288;   // (tiles_x + 1) * (tiles_y + 1): 1920x1080 needs 121 x 69
 constexpr int HIST_BITS = 10;            // depth-code histogram resolution (near/far split)
 constexpr int NHIST = 1 << HIST_BITS;
@@ -61,7 +60,8 @@ struct CamBatch {
 
 // A batch of B <= MAX_VB views is processed together, in two depth chunks (DESIGN.md §5 a3):
 // per-(view, Gaussian) arrays are [B*G], indexed by the batch index j = v*G + i.
-//   rec0 = (mean2d.x, mean2d.y, r, o)     rec1 = (qa, qb, qc, ycut)     rec2 = (box ext x, y, id, 0)
+//   rec0 = (mean2d.x, mean2d.y, r, o)     rec1 = (qa, qb, qc, ycut)
+//   rec2 = (box ext x, y, id, sy)         rec3 = span parameters (band_relevant)
 struct ViewBuffers {
     uint32_t* code;          // [B*G] depth code (bits(t_z) - bits(0.2f)), all ones = invisible
     uint32_t* hist;          // [B*NHIST] histogram of the codes' top bits, per view
@@ -79,7 +79,8 @@ struct ViewBuffers {
     uint2* rect;             // bin rect (bx0 | by0<<16, bx1 | by1<<16), exclusive ends
     float4* rec0;
     float4* rec1;
-    float4* rec2;            // (support box half-extents x, y, Gaussian id bits, 0)
+    float4* rec2;            // (support box half-extents x, y, Gaussian id bits, sy)
+    float4* rec3;            // (ky/(-qa), yc/(-qa), -qb/(2 qa), sx): band_relevant parameters
     float* Tstate;           // [B*H*W] per-pixel transmittance between chunks (0 = finished)
     uint8_t* tile_live;      // [B*tiles] 1 while a tile has an unfinished pixel
     uint8_t* flags;          // [B*G] far-chunk selection flags
@@ -89,7 +90,6 @@ struct ViewBuffers {
     uint32_t* ekey_alt;      // [E] sort scratch
     uint32_t* eval_alt;      // [E]
     uint2* ranges;           // [B*nbins] [begin, end) into the sorted entries
-    uint32_t* bin_count;     // [B*nbins] entries per bin (histogram of emission)
 };
 
 
@@ -102,6 +102,157 @@ enum DataErr : int { ERR_NONE = 0, ERR_GAUSSIAN = 1, ERR_REGION = 2, ERR_CODE = 
 
 __device__ __forceinline__ void latch_error(ErrorLatch e, int kind, long long idx) {
     if (atomicCAS(e.code, 0, kind) == 0) *e.index = idx;
+}
+
+// Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut; ext = support
+// box half-extents) produce a
+// fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r (square
+// support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative).  Margins make every
+// rounding here (and in the pixel's own fp32 evaluation of q, whose absolute error grows with
+// the size of the quadratic terms, e.g. for far off-screen near-plane Gaussians) only accept
+// more: the rectangle is widened by 0.5 px and ycut relaxed by 0.01 + 2e-6 * (bound on the
+// terms of q over the rectangle).  Chords use the Schur form (peak of q along a line,
+// 4 qa qc - qb^2 in fp64) so elongated ellipses do not lose precision.
+__device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float2 ext, float X0, float X1, float Y0, float Y1) {
+    const float mx = a.x, my = a.y, r = a.z;
+    // support box of preprocess (square support intersected with the alpha >= 1/255 ellipse's
+    // box, padded by >= 1 px): pixel centres outside it never produce a fragment
+    if (mx + ext.x < X0 || mx - ext.x > X1 || my + ext.y < Y0 || my - ext.y > Y1) return false;
+    const float M = 0.5f;
+    X0 -= M; X1 += M; Y0 -= M; Y1 += M;
+    // ellipse {q >= yc}: centre inside, or it meets an edge of the rectangle
+    if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
+    const float qa = b.x, qb = b.y, qc = b.z;
+    const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
+    const float dxm = fminf(fmaxf(fabsf(ex0), fabsf(ex1)), r), dym = fminf(fmaxf(fabsf(ey0), fabsf(ey1)), r);
+    const float mq = (fabsf(qa) + 0.5f * fabsf(qb)) * dxm * dxm + (fabsf(qc) + 0.5f * fabsf(qb)) * dym * dym;
+    const float yc = b.w - 0.01f - 2e-6f * mq;
+    const float dq = (float)(4.0 * (double)qa * (double)qc - (double)qb * (double)qb);
+    if (!(dq > 0.f)) return true;  // degenerate form: accept
+    const float ky = dq / (4.f * qa), kx = dq / (4.f * qc);  // peak of q along a row / column, per d^2
+    // rows y = const: q(dx) = qa (dx - c)^2 + ky dy^2 with c = -qb dy / (2 qa)
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const float ey = k ? ey1 : ey0;
+        const float h2 = (ky * ey * ey - yc) / -qa;
+        if (h2 >= 0.f) {
+            const float c = -qb * ey / (2.f * qa), h = sqrtf(h2);
+            if (c + h >= ex0 && c - h <= ex1) return true;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const float ex = k ? ex1 : ex0;
+        const float h2 = (kx * ex * ex - yc) / -qc;
+        if (h2 >= 0.f) {
+            const float c = -qb * ex / (2.f * qc), h = sqrtf(h2);
+            if (c + h >= ey0 && c - h <= ey1) return true;
+        }
+    }
+    return false;
+}
+
+// Tile-row spans of a Gaussian's possible fragments (GPU-only binning, DESIGN.md §5 a3).  For the
+// 16x16 tile row ty, row_span returns the tile columns [tx0, tx1] whose pixel centres may hold
+// a fragment: pixel centres inside the support box and inside the alpha >= 1/255 ellipse
+// {q >= yc} (yc relaxed as in rect_relevant, with the bound on q's terms taken over the whole
+// square support, so it is at least as loose).  Over the row's band (widened by 0.5 px) the
+// ellipse's x-extent is at its extreme points (+-sx, +-sy) when they lie in the band, else at
+// the band edge nearest to them (the right/left boundary is concave/convex in dy).  The same
+// function counts the entries (preprocess) and writes them (emit), so both agree exactly.
+struct Span {
+    float mx, my, bx, by;   // mean2d, support-box half-extents
+    float yc, ky, ia, cq;   // relaxed level, row-peak factor, 1/(-qa), -qb/(2 qa)
+    float sx, sy;           // rightmost point of the ellipse relative to the mean (leftmost: -sx, -sy)
+    bool box_only;          // degenerate form: use the box
+};
+
+__device__ __forceinline__ Span span_setup(float4 a, float4 b, float2 ext) {
+    Span s;
+    s.mx = a.x; s.my = a.y; s.bx = ext.x; s.by = ext.y;
+    const float r = a.z, qa = b.x, qb = b.y, qc = b.z;
+    const float mq = ((fabsf(qa) + fabsf(qc)) + fabsf(qb)) * r * r;
+    s.yc = b.w - 0.01f - 2e-6f * mq;
+    const double dq = 4.0 * (double)qa * (double)qc - (double)qb * (double)qb;
+    s.box_only = !(dq > 0.0) || !(qa < 0.f) || !(qc < 0.f) || !(s.yc < 0.f);
+    s.ky = (float)(dq / (4.0 * (double)qa));
+    s.ia = 1.0f / -qa;
+    s.cq = (float)(-(double)qb / (2.0 * (double)qa));
+    const double sxd = s.box_only ? 0.0 : sqrt(4.0 * (double)s.yc * (double)qc / dq);
+    s.sx = (float)sxd;
+    s.sy = s.box_only ? 0.f : (float)(-(double)qb / (2.0 * (double)qc) * sxd);
+    return s;
+}
+
+__device__ __forceinline__ void row_span(const Span& s, int ty, int tiles_x, int width, int height, int& tx0, int& tx1) {
+    tx0 = 1; tx1 = 0;  // empty
+    const float Y0 = (float)(ty * TILE) + 0.5f, Y1 = (float)(min(ty * TILE + TILE, height) - 1) + 0.5f;
+    if (s.my + s.by < Y0 || s.my - s.by > Y1) return;
+    float xl = s.mx - s.bx, xr = s.mx + s.bx;
+    if (!s.box_only) {
+        const float ey0 = Y0 - 0.5f - s.my, ey1 = Y1 + 0.5f - s.my;
+        float rr, ll;
+        if (s.sy >= ey0 && s.sy <= ey1) {
+            rr = s.sx;
+        } else {
+            const float ey = s.sy < ey0 ? ey0 : ey1;
+            const float h2 = (s.ky * ey * ey - s.yc) * s.ia;
+            if (h2 < 0.f) return;  // the band misses the (relaxed) ellipse
+            rr = s.cq * ey + sqrtf(h2);
+        }
+        if (-s.sy >= ey0 && -s.sy <= ey1) {
+            ll = -s.sx;
+        } else {
+            const float ey = -s.sy < ey0 ? ey0 : ey1;
+            const float h2 = (s.ky * ey * ey - s.yc) * s.ia;
+            if (h2 < 0.f) return;
+            ll = s.cq * ey - sqrtf(h2);
+        }
+        // outward margins: 0.5 px (as rect_relevant) + fp32 rounding of the terms above
+        const float mr = 0.5f + 1e-4f * (fabsf(rr) + fabsf(s.mx)) + 1e-3f;
+        const float ml = 0.5f + 1e-4f * (fabsf(ll) + fabsf(s.mx)) + 1e-3f;
+        xr = fminf(xr, s.mx + rr + mr);
+        xl = fmaxf(xl, s.mx + ll - ml);
+    }
+    if (!(xl <= xr)) return;
+    // pixels x whose centre x + 0.5 lies in [xl, xr]
+    const float fx0 = fmaxf(ceilf(xl - 0.5f), 0.f), fx1 = fminf(floorf(xr - 0.5f), (float)(width - 1));
+    if (!(fx0 <= fx1)) return;
+    tx0 = (int)fx0 >> 4;
+    tx1 = (int)fx1 >> 4;
+    (void)tiles_x;
+}
+
+// The same x-extent computation with the Span parameters precomputed in preprocess (rec2.w = sy,
+// rec3 = (ky/(-qa), yc/(-qa), -qb/(2 qa), sx), sx < 0: box only): may the Gaussian produce a
+// fragment at a pixel centre of [X0, X1] x [Y0, Y1]?  Used by the raster's per-tile and per-warp
+// filters (conservative; the exact decision is the per-pixel spec).
+__device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, float X0, float X1, float Y0, float Y1) {
+    const float mx = a.x, my = a.y;
+    if (mx + e2.x < X0 || mx - e2.x > X1 || my + e2.y < Y0 || my - e2.y > Y1) return false;
+    const float sx = e3.w, sy = e2.w;
+    if (!(sx > 0.f)) return true;
+    const float ey0 = Y0 - 0.5f - my, ey1 = Y1 + 0.5f - my;
+    float rr, ll;
+    if (sy >= ey0 && sy <= ey1) {
+        rr = sx;
+    } else {
+        const float ey = sy < ey0 ? ey0 : ey1;
+        const float h2 = e3.x * ey * ey - e3.y;
+        if (h2 < 0.f) return false;
+        rr = e3.z * ey + sqrtf(h2);
+    }
+    if (-sy >= ey0 && -sy <= ey1) {
+        ll = -sx;
+    } else {
+        const float ey = -sy < ey0 ? ey0 : ey1;
+        const float h2 = e3.x * ey * ey - e3.y;
+        if (h2 < 0.f) return false;
+        ll = e3.z * ey - sqrtf(h2);
+    }
+    const float mr = 0.5f + 1e-4f * (fabsf(rr) + fabsf(mx)) + 1e-3f;
+    const float ml = 0.5f + 1e-4f * (fabsf(ll) + fabsf(mx)) + 1e-3f;
+    return mx + rr + mr >= X0 && mx + ll - ml <= X1;
 }
 
 // ---- launchers (kernels.cu) ----
@@ -121,11 +272,11 @@ void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binn
 void launch_gather_scan_input(const uint32_t* sval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
                               cudaStream_t s);
 void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int key_bits, const uint64_t* offsets,
-                 const uint2* rect, Binning bn, int64_t n, int nviews, uint32_t* ekey, uint32_t* eval,
-                 uint32_t* bin_count, cudaStream_t s);
+                 const ViewBuffers& vb, const Binning& bn, int width, int height, int64_t n, int nviews,
+                 uint32_t* ekey, uint32_t* eval, cudaStream_t s);
+void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s);
 void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
                       const Binning& bn, uint8_t* flags, cudaStream_t s);
-void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s);
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K,
                          int L, uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s);
 
@@ -139,6 +290,7 @@ struct RasterParams {
     const float4* rec0;           // [nviews * G]
     const float4* rec1;
     const float4* rec2;
+    const float4* rec3;
     float* Tstate;                // [nviews * H*W] transmittance carried between chunks
     uint8_t* tile_live;           // [nviews * tiles]
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate

@@ -380,10 +380,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                     int y0 = (int)fmaxf(fy0, 0.f), y1 = (int)fminf(fy1, Hm1);
                     int tx0 = x0 >> bn.bshx, tx1 = (x1 >> bn.bshx) + 1, ty0 = y0 >> bn.bshy, ty1 = (y1 >> bn.bshy) + 1;
                     ntiles = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
+                    const float4 r0 = make_float4(mx, my, r, o), r1 = make_float4(qa, qb, qc, ycut);
+                    const float2 ext = make_float2(hx + padx, hy + pady);
+                    const Span sp = span_setup(r0, r1, ext);
                     vb.rect[e] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
-                    vb.rec0[e] = make_float4(mx, my, r, o);
-                    vb.rec1[e] = make_float4(qa, qb, qc, ycut);
-                    vb.rec2[e] = make_float4(hx + padx, hy + pady, __uint_as_float((uint32_t)i), 0.f);
+                    vb.rec0[e] = r0;
+                    vb.rec1[e] = r1;
+                    vb.rec2[e] = make_float4(ext.x, ext.y, __uint_as_float((uint32_t)i), sp.sy);
+                    vb.rec3[e] = make_float4(sp.ky * sp.ia, sp.yc * sp.ia, sp.cq, sp.box_only ? -1.f : sp.sx);
                 }
             }
         }
@@ -400,21 +404,16 @@ __global__ void gather_tiles_kernel(const uint32_t* __restrict__ sval_sorted, co
 }
 
 // ------------------------------------------------------------------ emit
-// Entry m of the element at sorted position k (chunk index e, view v = sorted key >> key_bits) goes
-// to slot offsets[k-1] + m
-// with key v*nbins + bin, so the entries are in (view, depth, index) order before the stable
-// bin sort.  Per-bin entry counts are accumulated through a shared-memory histogram (they give
-// the bin ranges directly).
+// Entry m of the element at sorted position k (chunk index e, view v = sorted key >> key_bits)
+// goes to slot offsets[k-1] + m: the m-th bin of its support rectangle, keyed v*nbins + bin.
+// The entries are in (view, depth, index) order before the stable bin sort, so each bin's list
+// is too; the raster filters its tile's candidates with band_relevant.
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ sval_sorted,
                                                    const uint32_t* __restrict__ skey_sorted, int key_bits,
                                                    const uint64_t* __restrict__ offsets,
                                                    const uint2* __restrict__ rect, int bins_x, int nbins, int64_t n,
-                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval,
-                                                   uint32_t* __restrict__ bin_count, int total_bins) {
-    __shared__ uint32_t hist[MAX_BINS];
-    for (int i = threadIdx.x; i < total_bins; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint64_t begin = 0, end = 0;
     uint32_t g = 0, kbase = 0;
@@ -433,10 +432,8 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     if (cnt > 0 && cnt <= SMALL) {
         const uint32_t bx0 = rc.x & 0xFFFFu, by0 = rc.x >> 16, w = (rc.y & 0xFFFFu) - bx0;
         for (uint32_t m = 0; m < cnt; m++) {
-            const uint32_t key = kbase + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
-            ekey[begin + m] = key;
+            ekey[begin + m] = kbase + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
             eval[begin + m] = g;
-            atomicAdd(&hist[key], 1u);
         }
     }
     unsigned big = __ballot_sync(0xffffffffu, cnt > SMALL);
@@ -450,35 +447,21 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
         const uint32_t skb = __shfl_sync(0xffffffffu, kbase, src);
         const uint32_t bx0 = rx & 0xFFFFu, by0 = rx >> 16, w = (ry & 0xFFFFu) - bx0;
         for (uint32_t m = lane; m < sc; m += 32) {
-            const uint32_t key = skb + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
-            ekey[sb + m] = key;
+            ekey[sb + m] = skb + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
             eval[sb + m] = sg;
-            atomicAdd(&hist[key], 1u);
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < total_bins; i += blockDim.x)
-        if (hist[i]) atomicAdd(&bin_count[i], hist[i]);
 }
 
-// Exclusive scan of the bin counts -> [begin, end) per bin (one CTA of 1024 threads, two bins
-// per thread, nbins <= MAX_BINS = 2048).
-__global__ void __launch_bounds__(1024) ranges_from_counts_kernel(const uint32_t* __restrict__ cnt, int nbins,
-                                                                  uint2* __restrict__ ranges) {
-    __shared__ uint32_t sc[1024];
-    const int t = threadIdx.x;
-    const uint32_t c0 = 2 * t < nbins ? cnt[2 * t] : 0u, c1 = 2 * t + 1 < nbins ? cnt[2 * t + 1] : 0u;
-    sc[t] = c0 + c1;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        uint32_t v = t >= o ? sc[t - o] : 0u;
-        __syncthreads();
-        sc[t] += v;
-        __syncthreads();
-    }
-    const uint32_t base = sc[t] - (c0 + c1);
-    if (2 * t < nbins) ranges[2 * t] = make_uint2(base, base + c0);
-    if (2 * t + 1 < nbins) ranges[2 * t + 1] = make_uint2(base + c0, base + c0 + c1);
+// Per-bin [begin, end) in the bin-sorted entries (ranges zeroed first; keys >= sentinel skipped).
+__global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t E, uint32_t sentinel,
+                              uint2* __restrict__ ranges) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const uint32_t key = keys[k];
+    if (key >= sentinel) return;
+    if (k == 0 || keys[k - 1] != key) ranges[key].x = (uint32_t)k;
+    if (k == E - 1 || keys[k + 1] != key) ranges[key].y = (uint32_t)(k + 1);
 }
 
 // ------------------------------------------------------------------ ingest codes
@@ -683,16 +666,19 @@ void launch_gather_scan_input(const uint32_t* sval_sorted, const uint32_t* tiles
 }
 
 void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int key_bits, const uint64_t* offsets,
-                 const uint2* rect, Binning bn, int64_t n, int nviews, uint32_t* ekey, uint32_t* eval,
-                 uint32_t* bin_count, cudaStream_t s) {
+                 const ViewBuffers& vb, const Binning& bn, int width, int height, int64_t n, int nviews,
+                 uint32_t* ekey, uint32_t* eval, cudaStream_t s) {
     if (n <= 0) return;
-    const int total_bins = nviews * bn.nbins();
-    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, skey_sorted, key_bits, offsets, rect, bn.bins_x,
-                                                 bn.nbins(), n, ekey, eval, bin_count, total_bins);
+    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, skey_sorted, key_bits, offsets, vb.rect, bn.bins_x,
+                                                 bn.nbins(), n, ekey, eval);
+    (void)nviews;
+    (void)width;
+    (void)height;
 }
 
-void launch_ranges_from_counts(const uint32_t* bin_count, int nbins, uint2* ranges, cudaStream_t s) {
-    ranges_from_counts_kernel<<<1, 1024, 0, s>>>(bin_count, nbins, ranges);
+void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s) {
+    if (E <= 0) return;
+    ranges_kernel<<<grid_for(E, 256), 256, 0, s>>>(keys_sorted, E, sentinel, ranges);
 }
 
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K, int L,

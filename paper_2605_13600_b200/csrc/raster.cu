@@ -35,6 +35,9 @@ constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // hash-table sentinel
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + BATCH)
 constexpr int NWARP = TILE_PIX / 32;
+#ifndef RGROUP
+#define RGROUP 4                              // records per warp-uniform branch in the pixel loop
+#endif
 
 // DESIGN.md §3 exp2_spec for ycut <= y <= 0 (the caller's conservative prune guarantees
 // y >= ycut > -64, so the oracle's y < -64 branch is unreachable here).
@@ -52,54 +55,6 @@ __device__ __forceinline__ float exp2_spec(float y) {
     p = __fmaf_rn(p, f, 1.0f);
     // ldexp(p, k): bits(t) << 23 == k << 23 (mod 2^32) for t = 1.5*2^23 + k
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-// Conservative test: may Gaussian (rec0 = mx, my, r, o; rec1 = qa, qb, qc, ycut; ext = support
-// box half-extents) produce a
-// fragment at a pixel centre inside [X0, X1] x [Y0, Y1]?  A fragment needs |d| <= r (square
-// support) and q(d) >= ycut (alpha >= 1/255, ycut already conservative).  Margins make every
-// rounding here (and in the pixel's own fp32 evaluation of q, whose absolute error grows with
-// the size of the quadratic terms, e.g. for far off-screen near-plane Gaussians) only accept
-// more: the rectangle is widened by 0.5 px and ycut relaxed by 0.01 + 2e-6 * (bound on the
-// terms of q over the rectangle).  Chords use the Schur form (peak of q along a line,
-// 4 qa qc - qb^2 in fp64) so elongated ellipses do not lose precision.
-__device__ __forceinline__ bool rect_relevant(float4 a, float4 b, float2 ext, float X0, float X1, float Y0, float Y1) {
-    const float mx = a.x, my = a.y, r = a.z;
-    // support box of preprocess (square support intersected with the alpha >= 1/255 ellipse's
-    // box, padded by >= 1 px): pixel centres outside it never produce a fragment
-    if (mx + ext.x < X0 || mx - ext.x > X1 || my + ext.y < Y0 || my - ext.y > Y1) return false;
-    const float M = 0.5f;
-    X0 -= M; X1 += M; Y0 -= M; Y1 += M;
-    // ellipse {q >= yc}: centre inside, or it meets an edge of the rectangle
-    if (mx >= X0 && mx <= X1 && my >= Y0 && my <= Y1) return true;
-    const float qa = b.x, qb = b.y, qc = b.z;
-    const float ex0 = X0 - mx, ex1 = X1 - mx, ey0 = Y0 - my, ey1 = Y1 - my;
-    const float dxm = fminf(fmaxf(fabsf(ex0), fabsf(ex1)), r), dym = fminf(fmaxf(fabsf(ey0), fabsf(ey1)), r);
-    const float mq = (fabsf(qa) + 0.5f * fabsf(qb)) * dxm * dxm + (fabsf(qc) + 0.5f * fabsf(qb)) * dym * dym;
-    const float yc = b.w - 0.01f - 2e-6f * mq;
-    const float dq = (float)(4.0 * (double)qa * (double)qc - (double)qb * (double)qb);
-    if (!(dq > 0.f)) return true;  // degenerate form: accept
-    const float ky = dq / (4.f * qa), kx = dq / (4.f * qc);  // peak of q along a row / column, per d^2
-    // rows y = const: q(dx) = qa (dx - c)^2 + ky dy^2 with c = -qb dy / (2 qa)
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        const float ey = k ? ey1 : ey0;
-        const float h2 = (ky * ey * ey - yc) / -qa;
-        if (h2 >= 0.f) {
-            const float c = -qb * ey / (2.f * qa), h = sqrtf(h2);
-            if (c + h >= ex0 && c - h <= ex1) return true;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        const float ex = k ? ex1 : ex0;
-        const float h2 = (kx * ex * ex - yc) / -qc;
-        if (h2 >= 0.f) {
-            const float c = -qb * ex / (2.f * qc), h = sqrtf(h2);
-            if (c + h >= ey0 && c - h <= ey1) return true;
-        }
-    }
-    return false;
 }
 
 // Sum e[i] over the lanes in the group (all lanes if !MASKED); lane l returns the sum for i = l.
@@ -148,8 +103,8 @@ struct __align__(16) Smem {
     // batch q_head .. q_head + BATCH - 1 is always contiguous
     float4 q0[QCAP + BATCH];   // (mx, my, r, o)
     float4 q1[QCAP + BATCH];   // (qa, qb, qc, ycut)
-    float2 q2[QCAP + BATCH];   // support-box half-extents
-    uint32_t qg[QCAP + BATCH]; // Gaussian id
+    float4 q2[QCAP + BATCH];   // (support-box half-extents x, y, Gaussian id, sy)
+    float4 q3[QCAP + BATCH];   // band_relevant parameters
     float acc[2][MAX_SLOTS * BATCH];
     float accZ[2][BATCH];
     uint32_t slot_key[MAX_SLOTS];
@@ -170,9 +125,9 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
     const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
-    const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
     const int64_t gtile = (int64_t)view * ntiles + tile;
     if (p.chunk > 0 && !p.tile_live[gtile]) return;  // every pixel finished in an earlier chunk
+    const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
     const uint2 range = p.ranges[view * p.bn.nbins() + bin];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wx0 = tx * TILE + 8 * (warp & 1), wy0 = ty * TILE + 4 * (warp >> 1);
@@ -257,21 +212,19 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     uint32_t q_head = 0, q_count = 0;
     int buf = 0;
     while (true) {
-        // ---- refill the ring with candidates relevant to this tile (stable compaction)
+        // ---- refill the ring with the next (up to) 256 entries of the tile's list
         while (q_count < (uint32_t)BATCH && cursor < range.y) {
             const uint32_t idx = cursor + t;
             bool acc = false;
-            uint32_t g = 0;
             float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
-            float2 r2 = make_float2(-1.f, -1.f);
+            float4 r2 = make_float4(-1.f, -1.f, 0.f, 0.f), r3 = make_float4(0.f, 0.f, 0.f, -1.f);
             if (idx < range.y) {
                 const uint32_t e = __ldg(p.eval + idx);  // chunk index of the Gaussian
                 r0 = __ldg(p.rec0 + e);
-                r1 = __ldg(p.rec1 + e);
-                const float4 r2e = __ldg(p.rec2 + e);
-                r2 = make_float2(r2e.x, r2e.y);
-                g = __float_as_uint(r2e.z);
-                acc = rect_relevant(r0, r1, r2, TX0, TX1, TY0, TY1);
+                r2 = __ldg(p.rec2 + e);
+                r3 = __ldg(p.rec3 + e);
+                acc = band_relevant(r0, r2, r3, TX0, TX1, TY0, TY1);
+                if (acc) r1 = __ldg(p.rec1 + e);
             }
             const unsigned bal = __ballot_sync(FULL, acc);
             if (lane == 0) sm.wcnt[warp] = __popc(bal);
@@ -285,15 +238,15 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             }
             if (acc) {
                 const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
-                sm.qg[pos] = g;
                 sm.q0[pos] = r0;
                 sm.q1[pos] = r1;
                 sm.q2[pos] = r2;
+                sm.q3[pos] = r3;
                 if (pos < (uint32_t)BATCH) {
-                    sm.qg[pos + QCAP] = g;
                     sm.q0[pos + QCAP] = r0;
                     sm.q1[pos + QCAP] = r1;
                     sm.q2[pos + QCAP] = r2;
+                    sm.q3[pos + QCAP] = r3;
                 }
             }
             q_count += tot;
@@ -307,7 +260,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
         if (!warp_done && (uint32_t)lane < n) {
-            rel = rect_relevant(sm.q0[q_head + lane], sm.q1[q_head + lane], sm.q2[q_head + lane], WX0, WX1, WY0, WY1);
+            rel = band_relevant(sm.q0[q_head + lane], sm.q2[q_head + lane], sm.q3[q_head + lane], WX0, WX1, WY0, WY1);
         }
         const unsigned mask = __ballot_sync(FULL, rel);
 
@@ -319,14 +272,22 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
         const float4* b0 = sm.q0 + q_head;
         const float4* b1 = sm.q1 + q_head;
+        // Records go in groups of RGROUP with one warp-uniform branch per group: inside a group
+        // there is no control flow, so the T-independent work of the next record (loads, q,
+        // exp2_spec) overlaps the T update of the current one.  A record outside the warp's
+        // mask is a no-op (its `sq` is false).
 #pragma unroll
-        for (int j = 0; j < BATCH; j++) {
-            e[j] = 0.f;
-            if (mask & (1u << j)) {
+        for (int j = 0; j < BATCH; j++) e[j] = 0.f;
+#pragma unroll
+        for (int g0 = 0; g0 < BATCH; g0 += RGROUP)
+        if ((mask >> g0) & ((1u << RGROUP) - 1u)) {
+#pragma unroll
+        for (int j = g0; j < g0 + RGROUP; j++) {
+            {
                 const float4 a = b0[j];  // mx, my, r, o
                 const float4 b = b1[j];  // qa, qb, qc, ycut
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
-                const bool sq = T > 0.f && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                const bool sq = ((mask >> j) & 1u) && T > 0.f && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
                 const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
                                           __fmul_rn(__fmul_rn(b.z, dy), dy));
                 const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
@@ -339,6 +300,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 tbits |= sq ? (1u << j) : 0u;
             }
         }
+        }
         const bool any = cbits != 0u;
         cnt += __popc(cbits);
         tests += __popc(tbits);
@@ -347,7 +309,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 #pragma unroll
             for (int j = 0; j < BATCH; j++) {
                 if (e[j] > 0.f)
-                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, sm.qg[q_head + j], e[j],
+                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, __float_as_uint(sm.q2[q_head + j].z), e[j],
                                   coded ? my_code_row : -1);
             }
         }
@@ -396,12 +358,12 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const float v = sm.acc[buf][q * BATCH + j];
                 const uint32_t a = sm.slot_atom[q][s];
                 if (v > 0.f && a != NONE)
-                    atomicAdd(Wm + (int64_t)sm.qg[q_head + j] * L + a,
+                    atomicAdd(Wm + (int64_t)__float_as_uint(sm.q2[q_head + j].z) * L + a,
                               __fmul_rn(sm.slot_coef[q][s], v));
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
-                if (z > 0.f) atomicAdd(p.Z + sm.qg[q_head + t], z);
+                if (z > 0.f) atomicAdd(p.Z + __float_as_uint(sm.q2[q_head + t].z), z);
             }
             // zero the other accumulator buffer (flushed one batch ago)
             for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[buf ^ 1][i] = 0.f;
