@@ -246,14 +246,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    for _ in range(args.warmup):
+    # first warm-up step with the instrumented kernel variant: the algorithmic work of one step
+    # (support tests, contributions) for the roofline numerator; the timed steps run uncounted
+    up.set_counters(True)
+    step()
+    torch.cuda.synchronize()
+    st0 = up.stats()  # one step's counters (reset at each step start)
+    up.set_counters(False)
+    for _ in range(args.warmup - 1):
         step()
     torch.cuda.synchronize()
-    st = up.stats()  # one step's counters (reset at each step start)
-    contrib_step = sum_over_ranks(st["contributions"])
-    tests_step = sum_over_ranks(st["support_tests"])
-    entries_step = sum_over_ranks(st["tile_entries"])
-    visible_step = sum_over_ranks(st["visible"])
+    contrib_step = sum_over_ranks(st0["contributions"])
+    tests_step = sum_over_ranks(st0["support_tests"])
+    entries_step = sum_over_ranks(st0["tile_entries"])
+    visible_step = sum_over_ranks(st0["visible"])
 
     up.set_timing(True)
     barrier()
@@ -281,7 +287,7 @@ def main():
     launches = max(1, tm["raster_launches"])
     ras_avg_s = tm["raster_ms"] / launches / 1e3
     # algorithmic lane-ops of one step (DESIGN.md §5 a4) over the raster time of one step
-    ops_step = OPS_PER_TEST * st["support_tests"] + (2 * cfg.S + 1) * st["contributions"]
+    ops_step = OPS_PER_TEST * st0["support_tests"] + (2 * cfg.S + 1) * st0["contributions"]
     ras_step_s = tm["raster_ms"] / args.steps / 1e3
     achieved = ops_step / ras_step_s / 1e12 if ras_step_s > 0 else 0.0
     traffic_view, traffic_src = measured_traffic()

@@ -71,7 +71,8 @@ typedef struct {
     int64_t tile_entries;   /* (Gaussian, tile) pairs binned */
     int64_t visible;        /* sum over views of Gaussians passing the projection culls */
     int64_t support_tests;  /* (pixel, Gaussian) pairs inside the Gaussian's square support
-                               tested while the pixel was still active (Eq. 2 work) */
+                               tested while the pixel was still active (Eq. 2 work); counted
+                               only while scoup_uplift_set_counters(h, 1) is on */
     int64_t kernel_launches;/* launches of this library's own kernels (CUB sort/scan excluded) */
     int64_t cub_launches;   /* CUB device-wide sort/scan calls */
 } scoup_stats;
@@ -154,6 +155,11 @@ scoup_status scoup_uplift_get_accumulators(scoup_uplift *h, float **W, float **Z
 
 /* Copy the counters (synchronises the stream; returns latched EDATA if any). */
 scoup_status scoup_uplift_get_stats(scoup_uplift *h, scoup_stats *out);
+
+/* Enable (1) / disable (0) counting of support tests (scoup_stats.support_tests) in the
+ * fused kernel; a slower instrumented variant, off by default.  Contributions are always
+ * counted. */
+scoup_status scoup_uplift_set_counters(scoup_uplift *h, int enable);
 
 /* Enable (1) / disable (0) per-kernel-class event timing; enabling clears the totals. */
 scoup_status scoup_uplift_set_timing(scoup_uplift *h, int enable);

@@ -45,7 +45,7 @@ class scoup_timing(C.Structure):
 
 EXPORTS = ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
-           "scoup_uplift_set_timing", "scoup_uplift_get_timing",
+           "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
            "scoup_uplift_free", "scoup_last_error", "scoup_version"]
 
 _lib = None
@@ -65,6 +65,7 @@ def lib():
         L.scoup_uplift_reset.argtypes = [P]
         L.scoup_uplift_get_accumulators.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(i64)]
         L.scoup_uplift_get_stats.argtypes = [P, C.POINTER(scoup_stats)]
+        L.scoup_uplift_set_counters.argtypes = [P, C.c_int]
         L.scoup_uplift_set_timing.argtypes = [P, C.c_int]
         L.scoup_uplift_get_timing.argtypes = [P, C.POINTER(scoup_timing)]
         L.scoup_uplift_free.argtypes = [P]
@@ -73,7 +74,7 @@ def lib():
         L.scoup_version.restype = C.c_char_p
         for name in ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
                      "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
-                     "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
+                     "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -150,6 +151,10 @@ def scoup_uplift_get_stats(h: int) -> dict:
     s = scoup_stats()
     _check(lib().scoup_uplift_get_stats(h, C.byref(s)))
     return {k: getattr(s, k) for k, _ in scoup_stats._fields_}
+
+
+def scoup_uplift_set_counters(h: int, enable: bool) -> None:
+    _check(lib().scoup_uplift_set_counters(h, 1 if enable else 0))
 
 
 def scoup_uplift_set_timing(h: int, enable: bool) -> None:

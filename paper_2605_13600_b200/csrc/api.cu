@@ -161,8 +161,9 @@ struct scoup_uplift {
     bool topk_pending = false;
     int64_t kernel_launches = 0, cub_launches = 0;
     double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
-    double near_frac = 0.1;             // near chunk: this fraction of each view's visible Gaussians
+    double near_frac = 0.05;             // near chunk: this fraction of each view's visible Gaussians
     int bin_shift = 6;                  // bins of 2^bin_shift px squares
+    bool count_tests = false;           // raster counts support tests (scoup_uplift_set_counters)
 };
 
 namespace {
@@ -507,6 +508,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.Tstate = b.Tstate;
     p.tile_live = b.tile_live;
     p.chunk = chunk;
+    p.count_tests = h->count_tests;
     for (int v = 0; v < c.nv; v++) {
         const int u = c.v0 + v;
         p.region_ids[v] = c.ids_dev[v];
@@ -932,6 +934,13 @@ scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
     } catch (const CudaError& e) {
         return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
     }
+}
+
+scoup_status scoup_uplift_set_counters(scoup_uplift* h, int enable) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    h->count_tests = enable != 0;
+    return SCOUP_OK;
 }
 
 scoup_status scoup_uplift_set_timing(scoup_uplift* h, int enable) {

@@ -294,6 +294,7 @@ struct RasterParams {
     float* Tstate;                // [nviews * H*W] transmittance carried between chunks
     uint8_t* tile_live;           // [nviews * tiles]
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate
+    bool count_tests;             // count support tests (slower variant; scoup_uplift_set_counters)
     const uint32_t* region_ids[MAX_VB];  // [H*W] per view
     int64_t code_row0[MAX_VB];
     int32_t num_regions[MAX_VB];

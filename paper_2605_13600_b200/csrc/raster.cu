@@ -120,6 +120,7 @@ struct __align__(16) Smem {
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 3
 #endif
+template <bool COUNT_TESTS>
 __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_kernel(const RasterParams p) {
     __shared__ Smem sm;
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 e[j] = con ? __fmul_rn(al, T) : 0.f;
                 T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
                 cbits |= con ? (1u << j) : 0u;
-                tbits |= sq ? (1u << j) : 0u;
+                if (COUNT_TESTS) tbits |= sq ? (1u << j) : 0u;
             }
         }
         }
@@ -382,16 +383,18 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 
     // contributions (terms of Eq. 5's sum) and support tests
     const unsigned c = __reduce_add_sync(FULL, cnt);
-    const unsigned ts = __reduce_add_sync(FULL, tests);
     if (lane == 0 && c) atomicAdd(&sm.contrib, (unsigned long long)c);
-    if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
+    if (COUNT_TESTS) {
+        const unsigned ts = __reduce_add_sync(FULL, tests);
+        if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
+    }
     __syncthreads();
     if (t == 0) {
         if (sm.contrib) {
             atomicAdd(p.contrib_ctr, sm.contrib);
             if (p.contrib_out[view]) atomicAdd(reinterpret_cast<unsigned long long*>(p.contrib_out[view]), sm.contrib);
         }
-        if (sm.tests) atomicAdd(p.support_ctr, sm.tests);
+        if (COUNT_TESTS && sm.tests) atomicAdd(p.support_ctr, sm.tests);
     }
 }
 
@@ -401,7 +404,10 @@ void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (ntiles <= 0) return;
     static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the static 48 KB window");
-    raster_aggregate_kernel<<<ntiles, TILE_PIX, 0, s>>>(p);
+    if (p.count_tests)
+        raster_aggregate_kernel<true><<<ntiles, TILE_PIX, 0, s>>>(p);
+    else
+        raster_aggregate_kernel<false><<<ntiles, TILE_PIX, 0, s>>>(p);
 }
 
 }  // namespace scoup

@@ -77,6 +77,9 @@ class SparseUplift:
     def stats(self) -> dict:
         return abi.scoup_uplift_get_stats(self._h)
 
+    def set_counters(self, enable: bool = True):
+        abi.scoup_uplift_set_counters(self._h, enable)
+
     def set_timing(self, enable: bool = True):
         abi.scoup_uplift_set_timing(self._h, enable)
 
