@@ -288,7 +288,10 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const float4 a = b0[j];  // mx, my, r, o
                 const float4 b = b1[j];  // qa, qb, qc, ycut
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
-                const bool sq = ((mask >> j) & 1u) && T > 0.f && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                // (a finished pixel, T == 0, needs no test of its own: its Tn = 0 < 1e-4 makes
+                // every later fragment a non-contributing stop that leaves T = 0)
+                const bool sq = ((mask >> j) & 1u) && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                const bool active = COUNT_TESTS && T > 0.f;
                 const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
                                           __fmul_rn(__fmul_rn(b.z, dy), dy));
                 const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
@@ -297,8 +300,8 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const bool con = pass && !(Tn < K_TMIN);
                 e[j] = con ? __fmul_rn(al, T) : 0.f;
                 T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
-                cbits |= con ? (1u << j) : 0u;
-                if (COUNT_TESTS) tbits |= sq ? (1u << j) : 0u;
+                if (con) cbits |= 1u << j;
+                if (COUNT_TESTS && sq && active) tbits |= 1u << j;
             }
         }
         }

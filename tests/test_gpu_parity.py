@@ -277,3 +277,44 @@ def test_depth_chunk_split_is_exact(dev, tiny_scene, tiny_oracle, near_frac, mon
     cfg, scene, maps, codes = tiny_scene
     res = run_gpu(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
     assert_parity(res, tiny_oracle, cfg.K)
+
+
+def _band(cam, y0, y1):
+    """Rows [y0, y1) of a view as a camera of its own (same rays, principal point shifted)."""
+    return synth.Camera(cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.width, y1 - y0, cam.world_to_camera)
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+def test_indoor_full_size_levels(dev, level):
+    """configs[2] at full size (1M Gaussians: 100 clusters + 10% shell, 988x731, Dirichlet(0.5)
+    codes) for each of its three nested region levels (32 / 128 / 512 regions), on 2 sampled
+    views: element-wise W/Z parity, exact contribution counts, Top-K code parity."""
+    cfg = synth.CONFIGS["indoor"]
+    scene = synth.make_scene(cfg, 0)
+    views = [3, 101]
+    maps = synth.make_region_maps_torch(cfg, torch.device("cuda"), level=level, seed=0, views=views)
+    maps = maps.cpu().numpy().view(np.uint32)
+    codes = synth.make_codes(cfg, level=level, seed=0, views=views)
+    cams = [scene.cameras[v] for v in views]
+    ora = oracle.uplift(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    ties = assert_parity(res, ora, cfg.K)
+    assert ties < 1e-3 * scene.gaussians.count
+
+
+def test_stress_full_size_row_band(dev):
+    """configs[4] at full scene size (6M heavily overlapping Gaussians, L=128, S=K=8, 1920-px
+    rows): the oracle's cost per full 1920x1080 view is minutes, so the sample is a 48-row band
+    of one view (the same rays; principal point shifted), run through the same batched, chunked
+    GPU path.  Element-wise parity over all 6M rows and exact counts."""
+    cfg = synth.CONFIGS["stress"]
+    scene = synth.make_scene(cfg, 0)
+    v, y0, y1 = 5, 516, 564
+    full = synth.make_region_maps_torch(cfg, torch.device("cuda"), seed=0, views=[v]).cpu().numpy().view(np.uint32)
+    maps = np.ascontiguousarray(full[:, y0:y1])
+    codes = synth.make_codes(cfg, seed=0, views=[v])
+    cams = [_band(scene.cameras[v], y0, y1)]
+    ora = oracle.uplift(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    assert ora[2].sum() > 1_000_000
+    res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    assert_parity(res, ora, cfg.K)
