@@ -209,24 +209,40 @@ def main():
     from paper_2605_13600_b200 import distributed as D
     my_views = D.views_for_rank(cfg.num_views, rank, world)
     cams = [scene.cameras[v] for v in my_views]
-    maps = synth.make_region_maps_torch(cfg, dev, seed=0, views=my_views)
-    codes_h = synth.make_codes(cfg, seed=0, views=my_views)
-    codes = synth.Codes(torch.from_numpy(codes_h.atoms.view(np.int32)).to(dev), torch.from_numpy(codes_h.coefs).to(dev),
-                        codes_h.row0, codes_h.num_regions)
+    # semantic levels (configs[2]: three nested levels) are fused into one raster pass
+    nlev = len(cfg.regions)
+    maps_l = [synth.make_region_maps_torch(cfg, dev, level=l, seed=0, views=my_views) for l in range(nlev)]
+    codes_hl = [synth.make_codes(cfg, level=l, seed=0, views=my_views) for l in range(nlev)]
+    codes_l = [synth.Codes(torch.from_numpy(c.atoms.view(np.int32)).to(dev), torch.from_numpy(c.coefs).to(dev),
+                           c.row0, c.num_regions) for c in codes_hl]
+    maps = maps_l[0]
     gd = synth.Gaussians(*[torch.from_numpy(a).to(dev) for a in (g.means, g.scales, g.rotations, g.opacities)])
     Npad = D.padded_rows(G, world)
     first_row, shard = D.row_shard(G, rank, world)
-    up = SparseUplift(gd, L, K, device=local, rows_padded=Npad)
+    up = SparseUplift(gd, L, K, device=local, rows_padded=Npad, levels=nlev)
     Ws = torch.empty((shard, L), dtype=torch.float32, device=dev) if world > 1 else None
     Zs = torch.empty((shard,), dtype=torch.float32, device=dev) if world > 1 else None
 
+    def add(u, m_l, c_l):
+        if nlev == 1:
+            u.add_views(cams, m_l[0], c_l[0])
+        else:
+            u.add_views(cams, m_l, c_l)
+
+    def finalize_all(u, out_atoms=None, out_coefs=None):
+        for lvl in range(nlev):
+            if world > 1:
+                Wl = u.W if nlev == 1 else u.W[lvl]
+                D.reduce_scatter_accumulators(Wl, u.Z, Ws, Zs)
+                u.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs, level=lvl,
+                           out_atoms=out_atoms, out_coefs=out_coefs)
+            else:
+                u.finalize(0, G, level=lvl, out_atoms=out_atoms, out_coefs=out_coefs)
+
     def step():
         up.reset()
-        up.add_views(cams, maps, codes)
-        if world > 1:
-            D.reduce_scatter_accumulators(up.W, up.Z, Ws, Zs)
-            return up.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs)
-        return up.finalize()
+        add(up, maps_l, codes_l)
+        finalize_all(up)
 
     def barrier():
         if world > 1:
@@ -287,7 +303,7 @@ def main():
     launches = max(1, tm["raster_launches"])
     ras_avg_s = tm["raster_ms"] / launches / 1e3
     # algorithmic lane-ops of one step (DESIGN.md §5 a4) over the raster time of one step
-    ops_step = OPS_PER_TEST * st0["support_tests"] + (2 * cfg.S + 1) * st0["contributions"]
+    ops_step = OPS_PER_TEST * st0["support_tests"] + (2 * nlev * cfg.S + 1) * st0["contributions"]
     ras_step_s = tm["raster_ms"] / args.steps / 1e3
     achieved = ops_step / ras_step_s / 1e12 if ras_step_s > 0 else 0.0
     traffic_view, traffic_src = measured_traffic()
@@ -296,24 +312,18 @@ def main():
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        maps_h = maps.cpu().pin_memory()
+        maps_hl = [m.cpu().pin_memory() for m in maps_l]
         g_h = synth.Gaussians(*[torch.from_numpy(a).pin_memory() for a in (g.means, g.scales, g.rotations, g.opacities)])
-        atoms_h = torch.empty((Npad if world == 1 else shard, K), dtype=torch.int32).pin_memory()
-        coefs_h = torch.empty((Npad if world == 1 else shard, K), dtype=torch.float32).pin_memory()
-        ca_h = torch.from_numpy(codes_h.atoms.view(np.int32)).pin_memory()
-        cc_h = torch.from_numpy(codes_h.coefs).pin_memory()
-        codes_hp = synth.Codes(ca_h, cc_h, codes_h.row0, codes_h.num_regions)
         nrows = G if world == 1 else shard
+        atoms_h = torch.empty((nrows, K), dtype=torch.int32).pin_memory()
+        coefs_h = torch.empty((nrows, K), dtype=torch.float32).pin_memory()
+        codes_hpl = [synth.Codes(torch.from_numpy(c.atoms.view(np.int32)).pin_memory(),
+                                 torch.from_numpy(c.coefs).pin_memory(), c.row0, c.num_regions) for c in codes_hl]
 
         def e2e_step():
-            u2 = SparseUplift(g_h, L, K, device=local, rows_padded=Npad)
-            u2.add_views(cams, maps_h, codes_hp)
-            if world > 1:
-                D.reduce_scatter_accumulators(u2.W, u2.Z, Ws, Zs)
-                u2.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs,
-                            out_atoms=atoms_h[:shard], out_coefs=coefs_h[:shard])
-            else:
-                u2.finalize(0, G, out_atoms=atoms_h[:G], out_coefs=coefs_h[:G])
+            u2 = SparseUplift(g_h, L, K, device=local, rows_padded=Npad, levels=nlev)
+            add(u2, maps_hl, codes_hpl)
+            finalize_all(u2, out_atoms=atoms_h, out_coefs=coefs_h)  # codes read back to the host
             u2.close()
 
         e2e_step()
@@ -326,8 +336,9 @@ def main():
         barrier()
         n_e2e = max(1, min(args.steps, 2))
         e2e_s = max_over_ranks((time.perf_counter() - t0) / n_e2e)
-        h2d = sum_over_ranks(maps_h.numel() * 4 + G * 44 + ca_h.numel() * 8)
-        d2h = sum_over_ranks(nrows * K * 8)
+        h2d = sum_over_ranks(sum(m.numel() for m in maps_hl) * 4 + G * 44 +
+                             sum(c.atoms.numel() for c in codes_hpl) * 8)
+        d2h = sum_over_ranks(nlev * nrows * K * 8)
         e2e = {"value": contrib_step / e2e_s, "unit": "contributions/s", "seconds_per_step": e2e_s,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
@@ -343,10 +354,11 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "gaussians": G, "views": cfg.num_views, "width": cfg.width,
-                       "height": cfg.height, "L": L, "S": cfg.S, "K": K, "regions_per_view": cfg.regions[0],
+                       "height": cfg.height, "L": L, "S": cfg.S, "K": K, "levels": nlev,
+                       "regions_per_view": list(cfg.regions),
                        "parallelism": f"view-sharded x{world} + reduce-scatter" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (region maps %.2f GB, W %.0f MB per GPU)" % (
-                           maps.numel() * 4 / 1e9, Npad * L * 4 / 1e6)},
+                           sum(m.numel() for m in maps_l) * 4 / 1e9, nlev * Npad * L * 4 / 1e6)},
             "contributions_per_step": int(contrib_step),
             "support_tests_per_step": int(tests_step),
             "bin_entries_per_step": int(entries_step),

@@ -42,7 +42,8 @@ extern "C" {
 #define SCOUP_NONE 0xFFFFFFFFu  /* unassigned pixel / empty code slot */
 #define SCOUP_MAX_L 256         /* implementation limits (EUNSUPPORTED beyond) */
 #define SCOUP_MAX_K 32
-#define SCOUP_MAX_S 16
+#define SCOUP_MAX_S 16          /* per call: num_levels * S <= SCOUP_MAX_S */
+#define SCOUP_MAX_LEVELS 4
 
 typedef struct scoup_uplift scoup_uplift; /* opaque */
 
@@ -109,6 +110,21 @@ scoup_status scoup_uplift_init(int device, void *cuda_stream, int64_t num_gaussi
                                int64_t rows_padded, scoup_uplift **out);
 
 /*
+ * Fused multi-level uplift.  The paper uplifts its three SAM levels
+ * (fine / medium / coarse) independently and renders them together; every level
+ * sees exactly the same fragments e_i(v,p) -- only the region maps and codes differ -- so one
+ * projection, sort and raster pass can feed all of them.  A handle made here holds num_levels
+ * accumulators: W [num_levels, rows_padded, L] (level-major, contiguous; caller-allocated or
+ * NULL) and one Z [rows_padded] (Z_i counts every fragment, whatever the region, so it is the
+ * same for all levels).  num_levels in 1..SCOUP_MAX_LEVELS; scoup_uplift_init is this with 1.
+ * Other arguments and errors as scoup_uplift_init.
+ */
+scoup_status scoup_uplift_init_levels(int device, void *cuda_stream, int64_t num_gaussians,
+                                      const float *means, const float *scales, const float *rotations,
+                                      const float *opacities, int32_t num_levels, int32_t L, int32_t K,
+                                      float *W, float *Z, int64_t rows_padded, scoup_uplift **out);
+
+/*
  * Rasterise `num_views` views and scatter-add their sparse codes (Eq. 5 / Algorithm 1
  * lines 5-12) into the handle's accumulators.  May be called any number of times.
  *  cameras      host [V]; all views of one call must share width/height.
@@ -131,6 +147,19 @@ scoup_status scoup_uplift_add_views(scoup_uplift *h, int32_t num_views, const sc
                                     const float *code_coefs, int32_t S, int64_t *contributions_out);
 
 /*
+ * scoup_uplift_add_views for a handle of num_levels levels (scoup_uplift_init_levels):
+ *  region_ids   host array of num_levels pointers, each [V,H,W] (device or host, as above);
+ *  code_row0    host [num_levels, V]; num_regions host [num_levels, V];
+ *  code_atoms / code_coefs  host arrays of num_levels pointers to each level's code table.
+ *  num_levels * S <= SCOUP_MAX_S.  A region-id data error names the level.
+ *  scoup_uplift_add_views is this with one level (ESTATE on a multi-level handle).
+ */
+scoup_status scoup_uplift_add_views_levels(scoup_uplift *h, int32_t num_views, const scoup_camera *cameras,
+                                           const uint32_t *const *region_ids, const int64_t *code_row0,
+                                           const int32_t *num_regions, const uint32_t *const *code_atoms,
+                                           const float *const *code_coefs, int32_t S, int64_t *contributions_out);
+
+/*
  * Eq. 6 on rows [first_row, first_row + num_rows): per Gaussian, order the accumulated
  * coefficients by (value desc, atom asc), keep the first K positive ones, divide by their
  * sum (Z_i cancels) and pad with (SCOUP_NONE, 0).  A row with W_i == 0 gives an
@@ -146,11 +175,17 @@ scoup_status scoup_uplift_finalize_topk(scoup_uplift *h, int64_t first_row, int6
                                         const float *W_rows, const float *Z_rows,
                                         uint32_t *out_atoms, float *out_coefs);
 
+/* scoup_uplift_finalize_topk on level `level` (0 .. num_levels-1) of a multi-level handle;
+ * scoup_uplift_finalize_topk is level 0.  EINVAL for a level out of range. */
+scoup_status scoup_uplift_finalize_topk_level(scoup_uplift *h, int32_t level, int64_t first_row, int64_t num_rows,
+                                              const float *W_rows, const float *Z_rows, uint32_t *out_atoms,
+                                              float *out_coefs);
+
 /* Zero the accumulators and counters and clear a latched error (stream-ordered). */
 scoup_status scoup_uplift_reset(scoup_uplift *h);
 
-/* Device pointers of the accumulators: W [rows_padded, L], Z [rows_padded] (Eq. 5 sums
- * without 1/Z_i, and Z_i of Eq. 3).  Any out-pointer may be NULL. */
+/* Device pointers of the accumulators: W [num_levels, rows_padded, L], Z [rows_padded] (Eq. 5
+ * sums without 1/Z_i, and Z_i of Eq. 3).  Any out-pointer may be NULL. */
 scoup_status scoup_uplift_get_accumulators(scoup_uplift *h, float **W, float **Z, int64_t *rows_padded);
 
 /* Copy the counters (synchronises the stream; returns latched EDATA if any). */

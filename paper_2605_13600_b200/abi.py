@@ -43,7 +43,8 @@ class scoup_timing(C.Structure):
                 ("topk_ms", C.c_double), ("raster_launches", C.c_int64), ("views_timed", C.c_int64)]
 
 
-EXPORTS = ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
+EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
+           "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
            "scoup_uplift_free", "scoup_last_error", "scoup_version"]
@@ -60,6 +61,9 @@ def lib():
         L = C.CDLL(LIB_PATH)
         P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         L.scoup_uplift_init.argtypes = [C.c_int, P, i64, P, P, P, P, i32, i32, P, P, i64, C.POINTER(P)]
+        L.scoup_uplift_init_levels.argtypes = [C.c_int, P, i64, P, P, P, P, i32, i32, i32, P, P, i64, C.POINTER(P)]
+        L.scoup_uplift_add_views_levels.argtypes = [P, i32, P, P, P, P, P, P, i32, P]
+        L.scoup_uplift_finalize_topk_level.argtypes = [P, i32, i64, i64, P, P, P, P]
         L.scoup_uplift_add_views.argtypes = [P, i32, P, P, P, P, P, P, i32, P]
         L.scoup_uplift_finalize_topk.argtypes = [P, i64, i64, P, P, P, P]
         L.scoup_uplift_reset.argtypes = [P]
@@ -72,7 +76,8 @@ def lib():
         L.scoup_uplift_free.restype = None
         L.scoup_last_error.restype = C.c_char_p
         L.scoup_version.restype = C.c_char_p
-        for name in ["scoup_uplift_init", "scoup_uplift_add_views", "scoup_uplift_finalize_topk",
+        for name in ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
+                     "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
                      "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
                      "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
             getattr(L, name).restype = C.c_int
@@ -120,6 +125,39 @@ def scoup_uplift_init(device: int, stream: int, num_gaussians: int, means, scale
                                    ptr(rotations), ptr(opacities), L, K, ptr(W), ptr(Z), rows_padded,
                                    C.byref(h)))
     return h.value
+
+
+def scoup_uplift_init_levels(device: int, stream: int, num_gaussians: int, means, scales, rotations, opacities,
+                             num_levels: int, L: int, K: int, W=None, Z=None, rows_padded: int = 0) -> int:
+    h = C.c_void_p()
+    _check(lib().scoup_uplift_init_levels(device, stream or None, num_gaussians, ptr(means), ptr(scales),
+                                          ptr(rotations), ptr(opacities), num_levels, L, K, ptr(W), ptr(Z),
+                                          rows_padded, C.byref(h)))
+    return h.value
+
+
+def _ptr_array(xs) -> C.Array:
+    arr = (C.c_void_p * len(xs))()
+    for i, x in enumerate(xs):
+        arr[i] = ptr(x)
+    return arr
+
+
+def scoup_uplift_add_views_levels(h: int, cameras: Sequence, region_ids: Sequence, code_row0, num_regions,
+                                  code_atoms: Sequence, code_coefs: Sequence, S: int, contributions_out=None) -> None:
+    """region_ids / code_atoms / code_coefs: one array per level; code_row0 / num_regions: [levels, V]."""
+    row0 = np.ascontiguousarray(code_row0, dtype=np.int64)
+    nreg = np.ascontiguousarray(num_regions, dtype=np.int32)
+    cams = cameras_struct(cameras)
+    ids, ats, cfs = _ptr_array(region_ids), _ptr_array(code_atoms), _ptr_array(code_coefs)
+    _check(lib().scoup_uplift_add_views_levels(h, len(cameras), cams, ids, ptr(row0), ptr(nreg), ats, cfs, S,
+                                               ptr(contributions_out)))
+
+
+def scoup_uplift_finalize_topk_level(h: int, level: int, first_row: int, num_rows: int, W_rows, Z_rows, out_atoms,
+                                     out_coefs) -> None:
+    _check(lib().scoup_uplift_finalize_topk_level(h, level, first_row, num_rows, ptr(W_rows), ptr(Z_rows),
+                                                  ptr(out_atoms), ptr(out_coefs)))
 
 
 def scoup_uplift_add_views(h: int, cameras: Sequence, region_ids, code_row0, num_regions, code_atoms,

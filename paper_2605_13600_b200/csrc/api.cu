@@ -121,7 +121,7 @@ struct Ctx {
     int64_t nsel = 0;
     bool far_any = false;
     CamBatch cams{};
-    const uint32_t* ids_dev[MAX_VB] = {};
+    const uint32_t* ids_dev[MAX_VB][MAX_LEV] = {};
     // timing: ring of event sets, 7 marks per batch (see ev_accumulate)
     struct EvSet { cudaEvent_t e[7]; bool pending; int views; };
     std::vector<EvSet> evs;
@@ -136,6 +136,7 @@ struct scoup_uplift {
     cudaStream_t stream = nullptr;
     int64_t G = 0, Npad = 0;
     int L = 0, K = 0;
+    int nlev = 1;  // semantic levels fused per pass; W is [nlev][Npad][L]
     float* W = nullptr;
     float* Z = nullptr;
     bool own_wz = false;
@@ -179,8 +180,12 @@ scoup_status check_latched(scoup_uplift* h) {
     h->latched = true;
     if (code == ERR_DEPTHKEY)
         return fail(SCOUP_ECUDA, "internal error: depth code beyond the batch bound at batch index " + std::to_string(idx));
+    if (code == ERR_REGION) {
+        const long long level = idx >> 48, pix = idx & ((1LL << 48) - 1);
+        return fail(SCOUP_EDATA, "data error: region id >= num_regions at flat pixel index " + std::to_string(pix) +
+                                     " (level " + std::to_string(level) + ")");
+    }
     const char* what = code == ERR_GAUSSIAN ? "non-finite or invalid Gaussian parameters at Gaussian index "
-                       : code == ERR_REGION ? "region id >= num_regions at flat pixel index "
                                             : "invalid code slot (atom >= L or bad coefficient) at flat slot index ";
     return fail(SCOUP_EDATA, std::string("data error: ") + what + std::to_string(idx));
 }
@@ -355,8 +360,9 @@ int depth_key_bits(const scoup_uplift* h, const Camera* cams, int n) {
 struct CallArgs {
     const Camera* cams;
     Binning bn;
-    const int64_t* code_row0;
-    const int32_t* num_regions;
+    const int64_t* code_row0;    // [nlev][V]: first row of (level, view) in the combined code table
+    const int32_t* num_regions;  // [nlev][V]
+    int V;
     int S;
     long long* contrib_out;
     int64_t npx;
@@ -509,11 +515,14 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.tile_live = b.tile_live;
     p.chunk = chunk;
     p.count_tests = h->count_tests;
+    p.nlev = h->nlev;
     for (int v = 0; v < c.nv; v++) {
         const int u = c.v0 + v;
-        p.region_ids[v] = c.ids_dev[v];
-        p.code_row0[v] = a.code_row0[u];
-        p.num_regions[v] = a.num_regions[u];
+        for (int l = 0; l < h->nlev; l++) {
+            p.region_ids[v][l] = c.ids_dev[v][l];
+            p.code_row0[v][l] = a.code_row0[(int64_t)l * a.V + u];
+            p.num_regions[v][l] = a.num_regions[(int64_t)l * a.V + u];
+        }
         p.pixel_base[v] = (long long)u * a.npx;
         p.contrib_out[v] = a.contrib_out ? a.contrib_out + u : nullptr;
     }
@@ -522,6 +531,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.S = a.S;
     p.L = h->L;
     p.W = h->W;
+    p.W_level_stride = h->Npad * (int64_t)h->L;
     p.Z = h->Z;
     p.contrib_ctr = h->d_stats + 1;
     p.support_ctr = h->d_stats + 4;
@@ -582,6 +592,14 @@ const char* scoup_version(void) { return "scoup-b200 0.1.0 (sm_100a)"; }
 scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussians, const float* means,
                                const float* scales, const float* rotations, const float* opacities, int32_t L,
                                int32_t K, float* W, float* Z, int64_t rows_padded, scoup_uplift** out) {
+    return scoup_uplift_init_levels(device, cuda_stream, num_gaussians, means, scales, rotations, opacities, 1, L, K,
+                                    W, Z, rows_padded, out);
+}
+
+scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num_gaussians, const float* means,
+                                      const float* scales, const float* rotations, const float* opacities,
+                                      int32_t num_levels, int32_t L, int32_t K, float* W, float* Z,
+                                      int64_t rows_padded, scoup_uplift** out) {
     g_last_error.clear();
     if (!out) return fail(SCOUP_EINVAL, "out is NULL");
     *out = nullptr;
@@ -591,6 +609,8 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
     if (K < 1) return fail(SCOUP_EINVAL, "K < 1");
     if (L < 1) return fail(SCOUP_EINVAL, "L < 1");
     if (K > L) return fail(SCOUP_EINVAL, "K > L (SPEC.md:291)");
+    if (num_levels < 1) return fail(SCOUP_EINVAL, "num_levels < 1");
+    if (num_levels > MAX_LEV) return fail(SCOUP_EUNSUPPORTED, "num_levels > SCOUP_MAX_LEVELS");
     if (L > SCOUP_MAX_L || K > SCOUP_MAX_K) return fail(SCOUP_EUNSUPPORTED, "L or K beyond implementation limits");
     if (num_gaussians >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "num_gaussians >= 2^31");
     if (rows_padded == 0) rows_padded = num_gaussians;
@@ -611,6 +631,7 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
         h->Npad = rows_padded;
         h->L = L;
         h->K = K;
+        h->nlev = num_levels;
         CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
         {
             cudaMemPool_t pool;
@@ -623,7 +644,7 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
             h->W = W;
             h->Z = Z;
         } else {
-            dalloc(&h->W, (size_t)std::max<int64_t>(1, rows_padded) * L, hs);
+            dalloc(&h->W, (size_t)std::max<int64_t>(1, rows_padded) * L * num_levels, hs);
             dalloc(&h->Z, (size_t)std::max<int64_t>(1, rows_padded), hs);
             h->own_wz = true;
         }
@@ -633,7 +654,7 @@ scoup_status scoup_uplift_init(int device, void* cuda_stream, int64_t num_gaussi
         CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
         CK(cudaMemsetAsync(h->d_err_index, 0, sizeof(long long), h->stream));
         CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
-        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * rows_padded * L, h->stream));
+        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * rows_padded * L * num_levels, h->stream));
         CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * rows_padded, h->stream));
         const int64_t G = std::max<int64_t>(1, num_gaussians);
         dalloc(&h->pg.a, G, hs);
@@ -706,17 +727,30 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
                                     const uint32_t* region_ids, const int64_t* code_row0, const int32_t* num_regions,
                                     const uint32_t* code_atoms, const float* code_coefs, int32_t S,
                                     int64_t* contributions_out) {
+    if (h && h->nlev != 1) return fail(SCOUP_ESTATE, "handle has several levels: use scoup_uplift_add_views_levels");
+    return scoup_uplift_add_views_levels(h, num_views, cameras, &region_ids, code_row0, num_regions, &code_atoms,
+                                         &code_coefs, S, contributions_out);
+}
+
+scoup_status scoup_uplift_add_views_levels(scoup_uplift* h, int32_t num_views, const scoup_camera* cameras,
+                                           const uint32_t* const* region_ids, const int64_t* code_row0,
+                                           const int32_t* num_regions, const uint32_t* const* code_atoms,
+                                           const float* const* code_coefs, int32_t S, int64_t* contributions_out) {
     g_last_error.clear();
     if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
     if (h->latched) return fail(SCOUP_ESTATE, "a latched data error is pending; call scoup_uplift_reset");
     if (num_views < 0) return fail(SCOUP_EINVAL, "num_views < 0");
     if (num_views == 0) return SCOUP_OK;
+    const int nlev = h->nlev;
     if (!cameras || !region_ids || !code_row0 || !num_regions || !code_atoms || !code_coefs)
         return fail(SCOUP_EINVAL, "NULL argument");
+    for (int l = 0; l < nlev; l++)
+        if (!region_ids[l] || !code_atoms[l] || !code_coefs[l]) return fail(SCOUP_EINVAL, "NULL level argument");
     if (S < 1) return fail(SCOUP_EINVAL, "S < 1");
     if (S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "S > SCOUP_MAX_S");
+    if (nlev * S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "num_levels * S > SCOUP_MAX_S");
     const int Wd = cameras[0].width, Hd = cameras[0].height;
-    int64_t rows = 0;
+    std::vector<int64_t> rows(nlev, 0), loff(nlev, 0);
     for (int v = 0; v < num_views; v++) {
         const scoup_camera& c = cameras[v];
         if (c.width != Wd || c.height != Hd) return fail(SCOUP_EINVAL, "cameras of one call must share width/height");
@@ -726,8 +760,11 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             return fail(SCOUP_EINVAL, "camera " + std::to_string(v) + ": bad intrinsics");
         if (!rigid_ok(c.world_to_camera))
             return fail(SCOUP_EDATA, "camera " + std::to_string(v) + ": world_to_camera is not rigid (1e-5)");
-        if (code_row0[v] < 0 || num_regions[v] < 0) return fail(SCOUP_EINVAL, "negative code_row0 / num_regions");
-        rows = std::max<int64_t>(rows, code_row0[v] + num_regions[v]);
+        for (int l = 0; l < nlev; l++) {
+            const int64_t k = (int64_t)l * num_views + v;
+            if (code_row0[k] < 0 || num_regions[k] < 0) return fail(SCOUP_EINVAL, "negative code_row0 / num_regions");
+            rows[l] = std::max<int64_t>(rows[l], code_row0[k] + num_regions[k]);
+        }
     }
     if ((int64_t)Wd * Hd >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "image too large");
     if ((int64_t)((Wd + TILE - 1) / TILE + 1) * ((Hd + TILE - 1) / TILE + 1) > MAX_SAT_ENTRIES)
@@ -735,11 +772,22 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
     if (h->G == 0) return SCOUP_OK;
     const Binning bn = choose_binning(Wd, Hd, h->bin_shift);
     const int64_t npx = (int64_t)Wd * Hd;
+    int64_t total_rows = 0;
+    for (int l = 0; l < nlev; l++) {
+        loff[l] = total_rows;
+        total_rows += rows[l];
+    }
+    // combined code table: level l's rows start at loff[l]
+    std::vector<int64_t> row0c((size_t)nlev * num_views);
+    for (int l = 0; l < nlev; l++)
+        for (int v = 0; v < num_views; v++)
+            row0c[(size_t)l * num_views + v] = loff[l] + code_row0[(int64_t)l * num_views + v];
     try {
         DeviceGuard dg(h->device);
-        // ---- codes: copy (if host) + validate + truncate (Algorithm 1 per-pixel TopK)
-        if (rows > 0) {
-            const size_t nslots = (size_t)(rows * S);
+        // ---- codes: copy every level into the combined table + validate + truncate
+        // (Algorithm 1 per-pixel TopK)
+        if (total_rows > 0) {
+            const size_t nslots = (size_t)(total_rows * S);
             if (nslots > h->code_cap) {
                 size_t cap = (size_t)((double)nslots * 1.25);
                 dfree(h->code_atoms, h->stream);
@@ -753,17 +801,18 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
                 dalloc(&h->code_coefs_in, cap, h->stream);
                 h->code_cap = cap;
             }
-            const uint32_t* ain = code_atoms;
-            const float* cin = code_coefs;
-            if (!is_device_ptr(code_atoms) || !is_device_ptr(code_coefs)) {
-                CK(cudaMemcpyAsync(h->code_atoms_in, code_atoms, sizeof(uint32_t) * nslots, cudaMemcpyDefault, h->stream));
-                CK(cudaMemcpyAsync(h->code_coefs_in, code_coefs, sizeof(float) * nslots, cudaMemcpyDefault, h->stream));
-                ain = h->code_atoms_in;
-                cin = h->code_coefs_in;
+            for (int l = 0; l < nlev; l++) {
+                if (rows[l] == 0) continue;
+                CK(cudaMemcpyAsync(h->code_atoms_in + loff[l] * S, code_atoms[l], sizeof(uint32_t) * rows[l] * S,
+                                   cudaMemcpyDefault, h->stream));
+                CK(cudaMemcpyAsync(h->code_coefs_in + loff[l] * S, code_coefs[l], sizeof(float) * rows[l] * S,
+                                   cudaMemcpyDefault, h->stream));
             }
-            launch_ingest_codes(ain, cin, rows, S, h->K, h->L, h->code_atoms, h->code_coefs, latch_of(h), h->stream);
+            launch_ingest_codes(h->code_atoms_in, h->code_coefs_in, total_rows, S, h->K, h->L, h->code_atoms,
+                                h->code_coefs, latch_of(h), h->stream);
         }
-        const bool ids_on_device = is_device_ptr(region_ids);
+        bool ids_on_device = true;
+        for (int l = 0; l < nlev; l++) ids_on_device = ids_on_device && is_device_ptr(region_ids[l]);
         std::vector<Camera> cams(num_views);
         for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
         // ---- view batches: up to MAX_VB views per pass (bounded by the bin table and by the
@@ -776,7 +825,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
             ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
         }
-        CallArgs args{cams.data(), bn, code_row0, num_regions, S, (long long*)contributions_out, npx};
+        CallArgs args{cams.data(), bn, row0c.data(), num_regions, num_views, S, (long long*)contributions_out, npx};
         int next = 0;  // first view not yet assigned to a batch
         auto start_batch = [&](Ctx& c) {
             int B = std::min(Bmax, num_views - next);
@@ -791,15 +840,18 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             c.nv = B;
             c.key_bits = kb;
             next += B;
-            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx), c.s, 1.0);
+            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx * nlev), c.s, 1.0);
             for (int v = 0; v < c.nv; v++) {
                 const int u = c.v0 + v;
-                if (ids_on_device) {
-                    c.ids_dev[v] = region_ids + (int64_t)u * npx;
-                } else {
-                    CK(cudaMemcpyAsync(c.ids_stage + (int64_t)v * npx, region_ids + (int64_t)u * npx,
-                                       sizeof(uint32_t) * npx, cudaMemcpyHostToDevice, c.s));
-                    c.ids_dev[v] = c.ids_stage + (int64_t)v * npx;
+                for (int l = 0; l < nlev; l++) {
+                    if (ids_on_device) {
+                        c.ids_dev[v][l] = region_ids[l] + (int64_t)u * npx;
+                    } else {
+                        uint32_t* dst = c.ids_stage + ((int64_t)l * Bmax + v) * npx;
+                        CK(cudaMemcpyAsync(dst, region_ids[l] + (int64_t)u * npx, sizeof(uint32_t) * npx,
+                                           cudaMemcpyHostToDevice, c.s));
+                        c.ids_dev[v][l] = dst;
+                    }
                 }
             }
             step_depth(h, c, args);
@@ -827,7 +879,7 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
             CK(cudaStreamWaitEvent(h->stream, h->ev_join[i], 0));
         }
         add_u64<<<1, 1, 0, h->stream>>>(h->d_stats + 0, (unsigned long long)num_views);
-        h->kernel_launches += 1 + (rows > 0 ? 1 : 0);
+        h->kernel_launches += 1 + (total_rows > 0 ? 1 : 0);
         CK(cudaGetLastError());
         if (st != SCOUP_OK) return st;
     } catch (const CudaError& e) {
@@ -839,16 +891,24 @@ scoup_status scoup_uplift_add_views(scoup_uplift* h, int32_t num_views, const sc
 
 scoup_status scoup_uplift_finalize_topk(scoup_uplift* h, int64_t first_row, int64_t num_rows, const float* W_rows,
                                         const float* Z_rows, uint32_t* out_atoms, float* out_coefs) {
+    return scoup_uplift_finalize_topk_level(h, 0, first_row, num_rows, W_rows, Z_rows, out_atoms, out_coefs);
+}
+
+scoup_status scoup_uplift_finalize_topk_level(scoup_uplift* h, int32_t level, int64_t first_row, int64_t num_rows,
+                                              const float* W_rows, const float* Z_rows, uint32_t* out_atoms,
+                                              float* out_coefs) {
     g_last_error.clear();
     (void)Z_rows;
     if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
     if (first_row < 0 || num_rows < 0) return fail(SCOUP_EINVAL, "negative row range");
+    if (level < 0 || level >= h->nlev) return fail(SCOUP_EINVAL, "level out of range");
     if (num_rows > 0 && (!out_atoms || !out_coefs)) return fail(SCOUP_EINVAL, "NULL output");
     if (!W_rows && first_row + num_rows > h->Npad) return fail(SCOUP_EINVAL, "row range beyond rows_padded");
     try {
         DeviceGuard dg(h->device);
         if (num_rows > 0) {
-            const float* Wsrc = W_rows ? W_rows : h->W + first_row * (int64_t)h->L;
+            const float* Wsrc =
+                W_rows ? W_rows : h->W + ((int64_t)level * h->Npad + first_row) * (int64_t)h->L;
             const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(num_rows, h->G - first_row));
             const bool dev_out = is_device_ptr(out_atoms) && is_device_ptr(out_coefs);
             uint32_t* da = out_atoms;
@@ -893,7 +953,7 @@ scoup_status scoup_uplift_reset(scoup_uplift* h) {
     if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
     try {
         DeviceGuard dg(h->device);
-        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * std::max<int64_t>(1, h->Npad) * h->L, h->stream));
+        CK(cudaMemsetAsync(h->W, 0, sizeof(float) * std::max<int64_t>(1, h->Npad) * h->L * h->nlev, h->stream));
         CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * std::max<int64_t>(1, h->Npad), h->stream));
         CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));

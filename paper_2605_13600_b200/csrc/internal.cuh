@@ -17,6 +17,7 @@ constexpr int BATCH = 32;                // Gaussians staged per raster batch
 constexpr int MAX_SLOTS = 32;            // distinct regions per tile on the smem-aggregated path
 constexpr int MAX_S = 16;
 constexpr int MAX_VB = 8;                // views batched per preprocess/sort/raster pass
+constexpr int MAX_LEV = 4;               // semantic levels fused per raster pass (nlev * S <= MAX_S)
 constexpr int MAX_SAT_ENTRIES = 12288;   // (tiles_x + 1) * (tiles_y + 1): 1920x1080 needs 121 x 69
 constexpr int HIST_BITS = 10;            // depth-code histogram resolution (near/far split)
 constexpr int NHIST = 1 << HIST_BITS;
@@ -224,12 +225,15 @@ __device__ __forceinline__ void row_span(const Span& s, int ty, int tiles_x, int
 }
 
 // The same x-extent computation with the Span parameters precomputed in preprocess (rec2.w = sy,
-// rec3 = (ky/(-qa), yc/(-qa), -qb/(2 qa), sx), sx < 0: box only): may the Gaussian produce a
-// fragment at a pixel centre of [X0, X1] x [Y0, Y1]?  Used by the raster's per-tile and per-warp
-// filters (conservative; the exact decision is the per-pixel spec).
-__device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, float X0, float X1, float Y0, float Y1) {
+// rec3 = (ky/(-qa), yc/(-qa), -qb/(2 qa), sx), sx < 0: box only): the pixel-centre x-interval
+// [xl, xr] where the Gaussian may produce a fragment within the pixel-centre rows [Y0, Y1]
+// (false: none).  Used by the raster's tile and warp filters (conservative; the exact decision
+// is the per-pixel spec).
+__device__ __forceinline__ bool band_extent(float4 a, float4 e2, float4 e3, float Y0, float Y1, float& xl, float& xr) {
     const float mx = a.x, my = a.y;
-    if (mx + e2.x < X0 || mx - e2.x > X1 || my + e2.y < Y0 || my - e2.y > Y1) return false;
+    if (my + e2.y < Y0 || my - e2.y > Y1) return false;
+    xl = mx - e2.x;
+    xr = mx + e2.x;
     const float sx = e3.w, sy = e2.w;
     if (!(sx > 0.f)) return true;
     const float ey0 = Y0 - 0.5f - my, ey1 = Y1 + 0.5f - my;
@@ -250,9 +254,14 @@ __device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, fl
         if (h2 < 0.f) return false;
         ll = e3.z * ey - sqrtf(h2);
     }
-    const float mr = 0.5f + 1e-4f * (fabsf(rr) + fabsf(mx)) + 1e-3f;
-    const float ml = 0.5f + 1e-4f * (fabsf(ll) + fabsf(mx)) + 1e-3f;
-    return mx + rr + mr >= X0 && mx + ll - ml <= X1;
+    xr = fminf(xr, mx + rr + 0.5f + 1e-4f * (fabsf(rr) + fabsf(mx)) + 1e-3f);
+    xl = fmaxf(xl, mx + ll - 0.5f - 1e-4f * (fabsf(ll) + fabsf(mx)) - 1e-3f);
+    return xl <= xr;
+}
+
+__device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, float X0, float X1, float Y0, float Y1) {
+    float xl, xr;
+    return band_extent(a, e2, e3, Y0, Y1, xl, xr) && xr >= X0 && xl <= X1;
 }
 
 // ---- launchers (kernels.cu) ----
@@ -295,16 +304,18 @@ struct RasterParams {
     uint8_t* tile_live;           // [nviews * tiles]
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate
     bool count_tests;             // count support tests (slower variant; scoup_uplift_set_counters)
-    const uint32_t* region_ids[MAX_VB];  // [H*W] per view
-    int64_t code_row0[MAX_VB];
-    int32_t num_regions[MAX_VB];
+    int nlev;                            // semantic levels fused in this pass (1..MAX_LEV)
+    const uint32_t* region_ids[MAX_VB][MAX_LEV];  // [H*W] per view and level
+    int64_t code_row0[MAX_VB][MAX_LEV];  // first row of (view, level) in the combined code table
+    int32_t num_regions[MAX_VB][MAX_LEV];
     long long pixel_base[MAX_VB];        // flat index of the view's first pixel (error reports)
     long long* contrib_out[MAX_VB];      // optional per-view counters
-    const uint32_t* code_atoms;   // sanitised table, rows of S slots
+    const uint32_t* code_atoms;   // sanitised combined table (all levels), rows of S slots
     const float* code_coefs;
     int S;
     int L;
-    float* W;
+    float* W;                     // [nlev][W_level_stride]
+    int64_t W_level_stride;       // rows_padded * L
     float* Z;
     unsigned long long* contrib_ctr;  // handle stats
     unsigned long long* support_ctr;  // handle stats: support tests

@@ -1,29 +1,31 @@
 // raster.cu -- fused rasterise-and-aggregate kernel (the hot loop of Algorithm 1).
 //
-// One CTA of 256 threads per 16x16 tile, one pixel per thread; warp w covers the 8x4 pixel
-// block at column 8*(w&1), row 4*(w>>1) of the tile (near-square blocks keep the number of
-// (warp, Gaussian) pairs low for small footprints).  The tile reads the depth-ordered Gaussian
-// list of the bin that contains it (bins are power-of-two groups of tiles) and
-// walks it front to back:
+// One CTA of 256 threads per (view, 16x16 tile), one pixel per thread; warp w covers the 8x4
+// pixel block at column 8*(w&1), row 4*(w>>1) of the tile (near-square blocks keep the number
+// of (warp, Gaussian) pairs low for small footprints).  The tile reads the depth-ordered
+// candidate list of the bin that contains it (bins are power-of-two squares of pixels,
+// DESIGN.md §5) and walks it front to back:
 //
-//  refill   256 candidates at a time are tested against the tile (square support and the
-//           alpha >= 1/255 ellipse, conservatively) and stably compacted into a shared-memory
+//  refill   256 candidates at a time are tested against the tile (support box and the ellipse
+//           band spans, conservatively, band_relevant) and stably compacted into a shared-memory
 //           ring of records, so the ring stays in (depth, index) order;
-//  batch    32 ring records at a time: each warp ballots the records whose support touches
-//           its 8x4 block (conservative) and, in order, every lane evaluates DESIGN.md §3 step
-//           PX on them -- square test, the log2-domain quadratic form, the q <= 0 guard,
-//           alpha = min(0.99, o exp2_spec(q)), the alpha >= 1/255 skip and the T(1-alpha) < 1e-4
-//           stop -- giving the weights e_i(v,p) = alpha_i T of PAPER.md Eq. 2,
-//           bit-identical to the CPU oracle.  Control flow is warp-uniform (one uniform branch
-//           per record); the per-lane decisions are predicates/selects.
+//  batch    32 ring records at a time: each warp ballots the records that may touch its 8x4 block
+//           (band_relevant) and, in order, every lane evaluates DESIGN.md §3 step PX on them -- square test, the
+//           log2-domain quadratic form, the q <= 0 guard, alpha = min(0.99, o exp2_spec(q)), the
+//           alpha >= 1/255 skip and the T(1-alpha) < 1e-4 stop -- giving the weights
+//           e_i(v,p) = alpha_i T of PAPER.md Eq. 2, bit-identical to the CPU oracle.
+//           Control flow is warp-uniform (one uniform branch per group of records); the
+//           per-lane decisions are predicates/selects.
 //
-// Aggregation (Eq. 5; Algorithm 1 lines 8-10): per warp and region
-// group, the per-pixel weights of the batch are summed with a 31-shuffle transpose-reduction
-// (lane l ends with the sum of the l-th evaluated Gaussian), the group sums of all warps are
-// combined per (tile region, Gaussian) in shared memory, and only then global reductions go
-// out: S `red.global.add.f32` per (tile region, Gaussian) into W[g][atom] (c * sum e) plus one
-// per Gaussian into Z[g].  A tile with more than MAX_SLOTS distinct regions falls back to
-// per-pixel reductions.
+// Aggregation (Eq. 5; Algorithm 1 lines 8-10), for all nlev semantic
+// levels of the pass at once (the levels share every fragment, only
+// the region maps differ): pixels are grouped by their tuple of region ids (one
+// per level) into at most MAX_SLOTS tile slots; per warp and slot group the per-pixel weights of
+// the batch are summed with a 31-shuffle transpose-reduction (lane l ends with the sum for the
+// l-th batch record), the group sums of all warps are combined per (slot, Gaussian) in shared
+// memory, and only then global reductions go out: nlev*S `red.global.add.f32` per
+// (slot, Gaussian) into W_level[g][atom] (c * sum e) plus one per Gaussian into Z[g].  A tile
+// with more than MAX_SLOTS distinct tuples falls back to per-pixel reductions.
 #include "internal.cuh"
 
 namespace scoup {
@@ -31,7 +33,7 @@ namespace scoup {
 namespace {
 
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;   // unassigned or outside the image
-constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // hash-table sentinel
+constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // slot-table sentinel
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + BATCH)
 constexpr int NWARP = TILE_PIX / 32;
@@ -85,31 +87,45 @@ __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool 
     return v[0];
 }
 
-// Fallback aggregation of one fragment (code_row < 0: unassigned pixel, Z only).
+// Fallback aggregation of one fragment: every level's code of the pixel (row < 0: unassigned at
+// that level, no W), and Z.  Scalars only, so the call needs no local-memory copies.
 __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* atoms, const float* coefs, int S,
-                                           int L, uint32_t g, float ev, int64_t code_row) {
+                                           int L, int nlev, int64_t level_stride, uint32_t g, float ev, int64_t r0,
+                                           int64_t r1, int64_t r2, int64_t r3) {
     atomicAdd(Z + g, ev);
-    if (code_row < 0) return;
-    for (int s = 0; s < S; s++) {
-        const uint32_t at = __ldg(atoms + code_row + s);
-        if (at != NONE) atomicAdd(W + (int64_t)g * L + at, __fmul_rn(__ldg(coefs + code_row + s), ev));
+    for (int l = 0; l < nlev; l++) {
+        const int64_t row = l == 0 ? r0 : l == 1 ? r1 : l == 2 ? r2 : r3;
+        if (row < 0) continue;
+        float* Wl = W + (int64_t)l * level_stride;
+        for (int s = 0; s < S; s++) {
+            const uint32_t at = __ldg(atoms + row + s);
+            if (at != NONE) atomicAdd(Wl + (int64_t)g * L + at, __fmul_rn(__ldg(coefs + row + s), ev));
+        }
     }
 }
 
 static_assert(BATCH == 32, "batch = one record per lane (transpose-reduction, flush indexing)");
 
-struct __align__(16) Smem {
+struct Ring {
     // ring of candidate records; slots [0, BATCH) are mirrored at [QCAP, QCAP + BATCH) so a
     // batch q_head .. q_head + BATCH - 1 is always contiguous
-    float4 q0[QCAP + BATCH];   // (mx, my, r, o)
-    float4 q1[QCAP + BATCH];   // (qa, qb, qc, ycut)
-    float4 q2[QCAP + BATCH];   // (support-box half-extents x, y, Gaussian id, sy)
-    float4 q3[QCAP + BATCH];   // band_relevant parameters
+    float4 q0[QCAP + BATCH];     // (mx, my, r, o)
+    float4 q1[QCAP + BATCH];     // (qa, qb, qc, ycut)
+    float4 q2[QCAP + BATCH];     // (support-box half-extents x, y, Gaussian id, sy)
+    float4 q3[QCAP + BATCH];     // band_relevant parameters
+};
+
+struct __align__(16) Smem {
+    union {
+        Ring r;
+        uint32_t stage[TILE_PIX][MAX_LEV];  // setup only: tuples proposed by the warps' group leaders
+    } u;
     float acc[2][MAX_SLOTS * BATCH];
     float accZ[2][BATCH];
-    uint32_t slot_key[MAX_SLOTS];
-    uint32_t slot_atom[MAX_SLOTS][MAX_S];
+    uint32_t slot_key[MAX_SLOTS][MAX_LEV];  // region id tuple of each slot
+    uint32_t slot_atom[MAX_SLOTS][MAX_S];   // per slot: nlev codes of S slots each
     float slot_coef[MAX_SLOTS][MAX_S];
+    int nstage;
     int wcnt[NWARP];
     int nslot;
     int overflow;
@@ -117,10 +133,13 @@ struct __align__(16) Smem {
     unsigned long long tests;
 };
 
+
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 3
 #endif
-template <bool COUNT_TESTS>
+// NLEV1: a single semantic level (the BASELINE configs' default), so that every level loop and
+// the tuple bookkeeping fold away; else 1..MAX_LEV levels from p.nlev.
+template <bool COUNT_TESTS, bool NLEV1>
 __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_kernel(const RasterParams p) {
     __shared__ Smem sm;
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
@@ -143,7 +162,11 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         }
         return;
     }
-    const int64_t code_row0 = p.code_row0[view];
+    const int nlev = NLEV1 ? 1 : p.nlev;
+    float4* const q0 = sm.u.r.q0;
+    float4* const q1 = sm.u.r.q1;
+    float4* const q2 = sm.u.r.q2;
+    float4* const q3 = sm.u.r.q3;
     // pixel-centre rectangles of the tile and of this warp's 8x4 block (clipped to the image)
     const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
     const float TX1 = (float)(min(tx * TILE + TILE, Wd) - 1) + 0.5f;
@@ -151,61 +174,105 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const float WX0 = (float)wx0 + 0.5f, WY0 = (float)wy0 + 0.5f;
     const float WX1 = (float)(min(wx0 + 8, Wd) - 1) + 0.5f, WY1 = (float)(min(wy0 + 4, Hd) - 1) + 0.5f;
 
-    // ---- setup: region key of my pixel, tile slot table, slot codes
-    uint32_t key = KEY_NONE;
-    if (inside) {
-        uint32_t rid = __ldg(p.region_ids[view] + (int64_t)y * Wd + x);
-        if (rid != NONE && rid >= (uint32_t)p.num_regions[view]) {
-            latch_error(p.err, ERR_REGION, p.pixel_base[view] + (int64_t)y * Wd + x);
-            rid = NONE;
+    // ---- setup: region id tuple of my pixel, tile slot table (distinct tuples), slot codes
+    uint32_t key[MAX_LEV];
+#pragma unroll
+    for (int l = 0; l < MAX_LEV; l++) {
+        key[l] = KEY_NONE;
+        if (l < nlev && inside) {
+            uint32_t rid = __ldg(p.region_ids[view][l] + (int64_t)y * Wd + x);
+            if (rid != NONE && rid >= (uint32_t)p.num_regions[view][l]) {
+                latch_error(p.err, ERR_REGION,
+                            ((long long)l << 48) + p.pixel_base[view] + (int64_t)y * Wd + x);
+                rid = NONE;
+            }
+            key[l] = rid;
         }
-        key = rid;
     }
-    if (t < MAX_SLOTS) sm.slot_key[t] = SLOT_EMPTY;
-    if (t == 0) { sm.nslot = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; }
+    if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; }
+    if (t < MAX_SLOTS) sm.slot_key[t][0] = SLOT_EMPTY;
     for (int i = t; i < 2 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
     if (t < 2 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
+    unsigned grp = FULL;
+#pragma unroll
+    for (int l = 0; l < MAX_LEV; l++)
+        if (l < nlev) grp &= __match_any_sync(FULL, key[l]);  // lanes with my whole tuple
     __syncthreads();
-    const unsigned grp = __match_any_sync(FULL, key);
-    const int leader = __ffs(grp) - 1;
-    int slot = -1;
-    if (lane == leader) {
-        for (int q = 0; q < MAX_SLOTS; q++) {
-            const uint32_t old = atomicCAS(&sm.slot_key[q], SLOT_EMPTY, key);
-            if (old == SLOT_EMPTY || old == key) { slot = q; break; }
+    int slot = 0;
+    if (NLEV1) {
+        // one region id per pixel: the warp's group leader claims (or finds) its slot by CAS
+        const int leader = __ffs(grp) - 1;
+        int sl = -1;
+        if (lane == leader) {
+            for (int q = 0; q < MAX_SLOTS; q++) {
+                const uint32_t old = atomicCAS(&sm.slot_key[q][0], SLOT_EMPTY, key[0]);
+                if (old == SLOT_EMPTY || old == key[0]) { sl = q; break; }
+            }
+            if (sl < 0) sm.overflow = 1;
+            else atomicMax(&sm.nslot, sl + 1);
         }
-        if (slot < 0) sm.overflow = 1;
-        else atomicMax(&sm.nslot, slot + 1);
+        slot = max(0, __shfl_sync(FULL, sl, leader));
+        __syncthreads();
+    } else {
+        if (lane == __ffs(grp) - 1) {  // one proposal per distinct tuple per warp
+            const int k = atomicAdd(&sm.nstage, 1);
+            for (int l = 0; l < MAX_LEV; l++) sm.u.stage[k][l] = key[l];
+        }
+        __syncthreads();
+        if (t == 0) {  // deduplicate the (few) proposals into the slot table
+            int ns = 0;
+            const int np = sm.nstage;
+            for (int k = 0; k < np; k++) {
+                int f = -1;
+                for (int q = 0; q < ns && f < 0; q++) {
+                    bool eq = true;
+                    for (int l = 0; l < nlev; l++) eq = eq && sm.slot_key[q][l] == sm.u.stage[k][l];
+                    if (eq) f = q;
+                }
+                if (f < 0) {
+                    if (ns == MAX_SLOTS) { sm.overflow = 1; break; }
+                    for (int l = 0; l < MAX_LEV; l++) sm.slot_key[ns][l] = sm.u.stage[k][l];
+                    ns++;
+                }
+            }
+            sm.nslot = ns;
+        }
+        __syncthreads();
+        if (!sm.overflow) {
+            for (int q = 0; q < sm.nslot; q++) {
+                bool eq = true;
+                for (int l = 0; l < nlev; l++) eq = eq && sm.slot_key[q][l] == key[l];
+                if (eq) { slot = q; break; }
+            }
+        }
     }
-    slot = __shfl_sync(FULL, slot, leader);
-    __syncthreads();
     const int nslot = sm.nslot;
     const bool overflow = sm.overflow != 0;
     const int S = p.S;
+    const int LS = nlev * S;  // W updates per (slot, Gaussian): every level's code
+    const int ls_log2 = (LS & (LS - 1)) == 0 ? __ffs(LS) - 1 : -1;
     const int s_log2 = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
-    for (int i = t; i < nslot * S; i += TILE_PIX) {
-        const int q = i / S, s = i - q * S;
-        const uint32_t k = sm.slot_key[q];
+    for (int i = t; i < nslot * LS; i += TILE_PIX) {
+        const int q = i / LS, ls = i - q * LS, l = ls / S, s = ls - l * S;
+        const uint32_t k = sm.slot_key[q][l];
         uint32_t a = NONE;
         float c = 0.f;
         if (k != KEY_NONE) {
-            const int64_t row = (code_row0 + (int64_t)k) * S + s;
+            const int64_t row = (p.code_row0[view][l] + (int64_t)k) * S + s;
             a = __ldg(p.code_atoms + row);
             c = __ldg(p.code_coefs + row);
         }
-        sm.slot_atom[q][s] = a;
-        sm.slot_coef[q][s] = c;
+        sm.slot_atom[q][ls] = a;
+        sm.slot_coef[q][ls] = c;
     }
-    // (slot codes are first read after a later barrier)
-    const bool coded = key != KEY_NONE;
-    const int64_t my_code_row = (code_row0 + (int64_t)(coded ? key : 0)) * S;
+    // (slot codes are first read after a later barrier; the ring overwrites the staging area
+    // only after the barrier of the first refill round)
 
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
     // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
     // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
     float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
     uint32_t cnt = 0, tests = 0;
-    float* Wm = p.W;
     const int L = p.L;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -213,7 +280,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     uint32_t q_head = 0, q_count = 0;
     int buf = 0;
     while (true) {
-        // ---- refill the ring with the next (up to) 256 entries of the tile's list
+        // ---- refill the ring: candidates with their warp masks (stable compaction)
         while (q_count < (uint32_t)BATCH && cursor < range.y) {
             const uint32_t idx = cursor + t;
             bool acc = false;
@@ -239,15 +306,15 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             }
             if (acc) {
                 const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
-                sm.q0[pos] = r0;
-                sm.q1[pos] = r1;
-                sm.q2[pos] = r2;
-                sm.q3[pos] = r3;
+                q0[pos] = r0;
+                q1[pos] = r1;
+                q2[pos] = r2;
+                q3[pos] = r3;
                 if (pos < (uint32_t)BATCH) {
-                    sm.q0[pos + QCAP] = r0;
-                    sm.q1[pos + QCAP] = r1;
-                    sm.q2[pos + QCAP] = r2;
-                    sm.q3[pos + QCAP] = r3;
+                    q0[pos + QCAP] = r0;
+                    q1[pos + QCAP] = r1;
+                    q2[pos + QCAP] = r2;
+                    q3[pos + QCAP] = r3;
                 }
             }
             q_count += tot;
@@ -257,26 +324,22 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         if (q_count == 0) break;
         const uint32_t n = min((uint32_t)BATCH, q_count);
 
-        // ---- per-warp mask of batch records touching this warp's 16x2 block
+        // ---- per-warp mask of batch records that may touch this warp's 8x4 block
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
-        if (!warp_done && (uint32_t)lane < n) {
-            rel = band_relevant(sm.q0[q_head + lane], sm.q2[q_head + lane], sm.q3[q_head + lane], WX0, WX1, WY0, WY1);
-        }
+        if (!warp_done && (uint32_t)lane < n)
+            rel = band_relevant(q0[q_head + lane], q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
         const unsigned mask = __ballot_sync(FULL, rel);
 
-        // ---- rasterise: e[j] for batch record j, in depth order (DESIGN.md §3 PX).  The branch
-        // on `mask` is warp-uniform; every lane computes the full sequence and the per-pixel
-        // decisions select the result (records outside the square or already-done pixels
-        // leave e[j] = 0 and T unchanged).
-        float e[BATCH];
-        uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
-        const float4* b0 = sm.q0 + q_head;
-        const float4* b1 = sm.q1 + q_head;
+        // ---- rasterise: e[j] for batch record j, in depth order (DESIGN.md §3 PX).
         // Records go in groups of RGROUP with one warp-uniform branch per group: inside a group
         // there is no control flow, so the T-independent work of the next record (loads, q,
         // exp2_spec) overlaps the T update of the current one.  A record outside the warp's
         // mask is a no-op (its `sq` is false).
+        float e[BATCH];
+        uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
+        const float4* b0 = q0 + q_head;
+        const float4* b1 = q1 + q_head;
 #pragma unroll
         for (int j = 0; j < BATCH; j++) e[j] = 0.f;
 #pragma unroll
@@ -309,17 +372,26 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         cnt += __popc(cbits);
         tests += __popc(tbits);
         if (overflow && any) {
-            // per-pixel reductions straight from the code table (tiles with > MAX_SLOTS regions)
+            // per-pixel reductions straight from the code table (tiles with > MAX_SLOTS tuples)
 #pragma unroll
             for (int j = 0; j < BATCH; j++) {
-                if (e[j] > 0.f)
-                    overflow_reds(Wm, p.Z, p.code_atoms, p.code_coefs, S, L, __float_as_uint(sm.q2[q_head + j].z), e[j],
-                                  coded ? my_code_row : -1);
+                if (e[j] > 0.f) {
+                    int64_t rw[MAX_LEV];  // my code rows (region ids re-read: a rare path)
+#pragma unroll
+                    for (int l = 0; l < MAX_LEV; l++) {
+                        uint32_t k = KEY_NONE;
+                        if (l < nlev) k = __ldg(p.region_ids[view][l] + (int64_t)y * Wd + x);
+                        rw[l] = (k != NONE && k < (uint32_t)p.num_regions[view][l])
+                                    ? (p.code_row0[view][l] + (int64_t)k) * S : -1;
+                    }
+                    overflow_reds(p.W, p.Z, p.code_atoms, p.code_coefs, S, L, nlev, p.W_level_stride,
+                                  __float_as_uint(q2[q_head + j].z), e[j], rw[0], rw[1], rw[2], rw[3]);
+                }
             }
         }
 
         if (!overflow) {
-            // ---- per (warp, region group) transpose-reduction, then shared accumulation
+            // ---- per (warp, slot group) transpose-reduction, then shared accumulation
             if (__any_sync(FULL, any)) {
                 // lane l ends with the group's sum for batch record l
                 const bool mine_rel = (mask >> lane) & 1u;
@@ -345,29 +417,31 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 }
             }
             __syncthreads();  // B1
-            // ---- flush: S reds per (slot, Gaussian) into W, one per Gaussian into Z
-            const int nitems = nslot * BATCH * S;
+            // ---- flush: nlev*S reds per (slot, Gaussian) into W_level, one per Gaussian into Z
+            const int nitems = nslot * BATCH * LS;
             for (int i = t; i < nitems; i += TILE_PIX) {
-                int q, j, s;
-                if (s_log2 >= 0) {  // S a power of two (every BASELINE config): shifts
-                    s = i & (S - 1);
-                    j = (i >> s_log2) & (BATCH - 1);
-                    q = i >> (s_log2 + 5);
+                int q, j, ls;
+                if (ls_log2 >= 0) {  // nlev * S a power of two (every single-level BASELINE config)
+                    ls = i & (LS - 1);
+                    j = (i >> ls_log2) & (BATCH - 1);
+                    q = i >> (ls_log2 + 5);
                 } else {
-                    q = i / (BATCH * S);
-                    const int rem = i - q * (BATCH * S);
-                    j = rem / S;
-                    s = rem - j * S;
+                    q = i / (BATCH * LS);
+                    const int rem = i - q * (BATCH * LS);
+                    j = rem / LS;
+                    ls = rem - j * LS;
                 }
                 const float v = sm.acc[buf][q * BATCH + j];
-                const uint32_t a = sm.slot_atom[q][s];
-                if (v > 0.f && a != NONE)
-                    atomicAdd(Wm + (int64_t)__float_as_uint(sm.q2[q_head + j].z) * L + a,
-                              __fmul_rn(sm.slot_coef[q][s], v));
+                const uint32_t a = sm.slot_atom[q][ls];
+                if (v > 0.f && a != NONE) {
+                    const int l = s_log2 >= 0 ? ls >> s_log2 : ls / S;
+                    atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
+                              __fmul_rn(sm.slot_coef[q][ls], v));
+                }
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
-                if (z > 0.f) atomicAdd(p.Z + __float_as_uint(sm.q2[q_head + t].z), z);
+                if (z > 0.f) atomicAdd(p.Z + __float_as_uint(q2[q_head + t].z), z);
             }
             // zero the other accumulator buffer (flushed one batch ago)
             for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[buf ^ 1][i] = 0.f;
@@ -407,10 +481,17 @@ void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (ntiles <= 0) return;
     static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the static 48 KB window");
-    if (p.count_tests)
-        raster_aggregate_kernel<true><<<ntiles, TILE_PIX, 0, s>>>(p);
-    else
-        raster_aggregate_kernel<false><<<ntiles, TILE_PIX, 0, s>>>(p);
+    if (p.nlev == 1) {
+        if (p.count_tests)
+            raster_aggregate_kernel<true, true><<<ntiles, TILE_PIX, 0, s>>>(p);
+        else
+            raster_aggregate_kernel<false, true><<<ntiles, TILE_PIX, 0, s>>>(p);
+    } else {
+        if (p.count_tests)
+            raster_aggregate_kernel<true, false><<<ntiles, TILE_PIX, 0, s>>>(p);
+        else
+            raster_aggregate_kernel<false, false><<<ntiles, TILE_PIX, 0, s>>>(p);
+    }
 }
 
 }  // namespace scoup

@@ -22,10 +22,11 @@ def _torch():
 
 
 class SparseUplift:
-    """One semantic level's uplift on one device (Algorithm 1)."""
+    """Uplift of one or several fused semantic levels on one device (Algorithm 1,
+    P:347-372; levels > 1: SURVEY.md §8(f) NEXT-1, one raster pass feeds every level)."""
 
     def __init__(self, gaussians, L: int, K: int, device: int = 0, rows_padded: int = 0,
-                 stream=None):
+                 stream=None, levels: int = 1):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("SparseUplift needs a CUDA device (there is no CPU fallback)")
@@ -35,12 +36,14 @@ class SparseUplift:
         self.G = G
         self.rows_padded = int(rows_padded) if rows_padded else G
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.W = torch.empty((max(1, self.rows_padded), self.L), dtype=torch.float32, device=self.device)
+        self.levels = int(levels)
+        shape = (max(1, self.rows_padded), self.L) if self.levels == 1 else (self.levels, max(1, self.rows_padded), self.L)
+        self.W = torch.empty(shape, dtype=torch.float32, device=self.device)
         self.Z = torch.empty((max(1, self.rows_padded),), dtype=torch.float32, device=self.device)
         keep = [self._as_input(a) for a in (gaussians.means, gaussians.scales, gaussians.rotations,
                                             gaussians.opacities)]
-        self._h = abi.scoup_uplift_init(device, self.stream.cuda_stream, G, *keep, self.L, self.K,
-                                        self.W, self.Z, self.rows_padded)
+        self._h = abi.scoup_uplift_init_levels(device, self.stream.cuda_stream, G, *keep, self.levels, self.L,
+                                               self.K, self.W, self.Z, self.rows_padded)
         self._keep = keep  # device inputs must outlive the stream point of init
 
     def _as_input(self, a):
@@ -51,16 +54,30 @@ class SparseUplift:
 
     def add_views(self, cameras: Sequence, region_ids, codes, contributions_out=None):
         """region_ids: [V,H,W] uint32 numpy (host) or int32/uint32 torch tensor (device or host).
-        codes: synth.Codes-like (atoms [rows,S] u32, coefs [rows,S] f32, row0 [V], num_regions [V])."""
-        atoms = codes.atoms if not isinstance(codes.atoms, np.ndarray) else np.ascontiguousarray(codes.atoms, np.uint32)
-        coefs = codes.coefs if not isinstance(codes.coefs, np.ndarray) else np.ascontiguousarray(codes.coefs, np.float32)
-        S = int(atoms.shape[1])
-        abi.scoup_uplift_add_views(self._h, list(cameras), region_ids, codes.row0, codes.num_regions,
-                                   atoms, coefs, S, contributions_out)
+        codes: synth.Codes-like (atoms [rows,S] u32, coefs [rows,S] f32, row0 [V], num_regions [V]).
+        With levels > 1: a sequence of per-level region maps and a sequence of per-level codes."""
+        def prep(c):
+            atoms = c.atoms if not isinstance(c.atoms, np.ndarray) else np.ascontiguousarray(c.atoms, np.uint32)
+            coefs = c.coefs if not isinstance(c.coefs, np.ndarray) else np.ascontiguousarray(c.coefs, np.float32)
+            return atoms, coefs
+        if self.levels == 1:
+            atoms, coefs = prep(codes)
+            S = int(atoms.shape[1])
+            abi.scoup_uplift_add_views(self._h, list(cameras), region_ids, codes.row0, codes.num_regions,
+                                       atoms, coefs, S, contributions_out)
+            return
+        if len(region_ids) != self.levels or len(codes) != self.levels:
+            raise ValueError(f"expected {self.levels} region maps and code tables")
+        pc = [prep(c) for c in codes]
+        S = int(pc[0][0].shape[1])
+        row0 = np.stack([np.asarray(c.row0, np.int64) for c in codes])
+        nreg = np.stack([np.asarray(c.num_regions, np.int32) for c in codes])
+        abi.scoup_uplift_add_views_levels(self._h, list(cameras), list(region_ids), row0, nreg,
+                                          [a for a, _ in pc], [c for _, c in pc], S, contributions_out)
 
     def finalize(self, first_row: int = 0, num_rows: Optional[int] = None, W_rows=None, Z_rows=None,
-                 out_atoms=None, out_coefs=None):
-        """Eq. 6 on rows [first_row, first_row+num_rows).  Returns (atoms u32->int32 view, coefs)."""
+                 out_atoms=None, out_coefs=None, level: int = 0):
+        """Eq. 6 on rows [first_row, first_row+num_rows) of `level`.  Returns (atoms u32->int32 view, coefs)."""
         torch = _torch()
         if num_rows is None:
             num_rows = (W_rows.shape[0] if W_rows is not None else self.G - first_row)
@@ -68,7 +85,8 @@ class SparseUplift:
             out_atoms = torch.empty((num_rows, self.K), dtype=torch.int32, device=self.device)
         if out_coefs is None:
             out_coefs = torch.empty((num_rows, self.K), dtype=torch.float32, device=self.device)
-        abi.scoup_uplift_finalize_topk(self._h, first_row, num_rows, W_rows, Z_rows, out_atoms, out_coefs)
+        abi.scoup_uplift_finalize_topk_level(self._h, level, first_row, num_rows, W_rows, Z_rows, out_atoms,
+                                             out_coefs)
         return out_atoms, out_coefs
 
     def reset(self):

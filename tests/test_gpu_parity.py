@@ -284,22 +284,93 @@ def _band(cam, y0, y1):
     return synth.Camera(cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.width, y1 - y0, cam.world_to_camera)
 
 
-@pytest.mark.parametrize("level", [0, 1, 2])
-def test_indoor_full_size_levels(dev, level):
+def run_gpu_levels(g, cams, maps_by_level, codes_by_level, L, K):
+    """Fused multi-level uplift (one raster pass for every level) through the C ABI."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    V, M = len(cams), len(maps_by_level)
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    ids = [torch.from_numpy(np.ascontiguousarray(m).view(np.int32)).cuda() for m in maps_by_level]
+    cods = [synth.Codes(torch.from_numpy(np.ascontiguousarray(c.atoms).view(np.int32)).cuda(),
+                        torch.from_numpy(np.ascontiguousarray(c.coefs)).cuda(), c.row0, c.num_regions)
+            for c in codes_by_level]
+    contrib = torch.zeros(V, dtype=torch.int64, device="cuda")
+    up = SparseUplift(gin, L, K, levels=M)
+    try:
+        up.add_views(cams, ids, cods, contributions_out=contrib)
+        out = []
+        for lvl in range(M):
+            atoms, coefs = up.finalize(level=lvl)
+            out.append((atoms.cpu().numpy().view(np.uint32), coefs.cpu().numpy()))
+        torch.cuda.synchronize()
+        W = up.W[:, :g.count].double().cpu().numpy()
+        Z = up.Z[:g.count].double().cpu().numpy()
+        return dict(W=W, Z=Z, codes=out, contrib=contrib.cpu().numpy(), stats=up.stats())
+    finally:
+        up.close()
+
+
+def assert_levels_parity(res, oras, K):
+    for lvl, ora in enumerate(oras):
+        r = dict(W=res["W"][lvl], Z=res["Z"], atoms=res["codes"][lvl][0], coefs=res["codes"][lvl][1],
+                 contrib=res["contrib"], stats=res["stats"])
+        assert_parity(r, ora, K)
+
+
+def test_fused_levels_tiny(dev):
+    """three nested region levels (8 / 32 / 128 regions, 10% of them
+    unassigned) fused into one raster pass equal three separate oracle uplifts: W per level, one
+    shared Z (it counts every fragment), codes per level, exact counts."""
+    cfg = synth.CONFIGS["tiny"].with_(regions=(8, 32, 128), unassigned_frac=0.1)
+    scene = synth.make_scene(cfg, 7)
+    maps = [synth.make_region_maps_numpy(cfg, level=l, seed=7) for l in range(3)]
+    codes = [synth.make_codes(cfg, level=l, seed=7) for l in range(3)]
+    oras = [oracle.uplift(scene.gaussians, scene.cameras, maps[l], codes[l], cfg.L, cfg.K) for l in range(3)]
+    res = run_gpu_levels(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    assert_levels_parity(res, oras, cfg.K)
+
+
+def test_fused_levels_indoor_full_size(dev):
     """configs[2] at full size (1M Gaussians: 100 clusters + 10% shell, 988x731, Dirichlet(0.5)
-    codes) for each of its three nested region levels (32 / 128 / 512 regions), on 2 sampled
-    views: element-wise W/Z parity, exact contribution counts, Top-K code parity."""
+    codes), its three nested levels (32 / 128 / 512 regions) fused in one pass, on 2 sampled
+    views: element-wise W/Z parity for every level, exact contribution counts, Top-K parity."""
     cfg = synth.CONFIGS["indoor"]
     scene = synth.make_scene(cfg, 0)
     views = [3, 101]
-    maps = synth.make_region_maps_torch(cfg, torch.device("cuda"), level=level, seed=0, views=views)
-    maps = maps.cpu().numpy().view(np.uint32)
-    codes = synth.make_codes(cfg, level=level, seed=0, views=views)
+    maps = [synth.make_region_maps_torch(cfg, torch.device("cuda"), level=l, seed=0, views=views)
+            .cpu().numpy().view(np.uint32) for l in range(3)]
+    codes = [synth.make_codes(cfg, level=l, seed=0, views=views) for l in range(3)]
     cams = [scene.cameras[v] for v in views]
-    ora = oracle.uplift(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
-    res = run_gpu(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
-    ties = assert_parity(res, ora, cfg.K)
-    assert ties < 1e-3 * scene.gaussians.count
+    oras = [oracle.uplift(scene.gaussians, cams, maps[l], codes[l], cfg.L, cfg.K) for l in range(3)]
+    res = run_gpu_levels(scene.gaussians, cams, maps, codes, cfg.L, cfg.K)
+    assert_levels_parity(res, oras, cfg.K)
+    # the single-level path on the finest level agrees too
+    single = run_gpu(scene.gaussians, cams, maps[2], codes[2], cfg.L, cfg.K)
+    assert_parity(single, oras[2], cfg.K)
+
+
+def test_fused_levels_errors(dev, tiny_scene):
+    """A bad region id names its level; the level count is bounded (SCOUP_MAX_LEVELS = 4,
+    levels * S <= SCOUP_MAX_S); finalize on a missing level is EINVAL."""
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    up = SparseUplift(scene.gaussians, cfg.L, cfg.K, levels=2)
+    try:
+        bad = maps[:1].copy()
+        bad[0, 5, 7] = 777
+        up.add_views(scene.cameras[:1], [maps[:1], bad], [codes, codes])
+        with pytest.raises(abi.ScoupError) as ei:
+            up.finalize()
+        assert ei.value.status == 2 and "level 1" in str(ei.value) and str(5 * 64 + 7) in str(ei.value)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.finalize(level=2)
+        assert ei.value.status == 1
+    finally:
+        up.close()
+    with pytest.raises(abi.ScoupError) as ei:
+        SparseUplift(scene.gaussians, cfg.L, cfg.K, levels=5)
+    assert ei.value.status == 6
 
 
 def test_stress_full_size_row_band(dev):
