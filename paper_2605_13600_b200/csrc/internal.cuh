@@ -14,7 +14,7 @@ constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int TILE = 16;                 // 16x16 pixel tiles, one CTA (256 threads) each
 constexpr int TILE_PIX = TILE * TILE;
 constexpr int BATCH = 32;                // Gaussians staged per raster batch
-constexpr int MAX_SLOTS = 32;            // distinct regions per tile on the smem-aggregated path
+constexpr int MAX_SLOTS = 16;            // distinct region(-tuple)s per tile on the smem-aggregated path
 constexpr int MAX_S = 16;
 constexpr int MAX_VB = 8;                // views batched per preprocess/sort/raster pass
 constexpr int MAX_LEV = 4;               // semantic levels fused per raster pass (nlev * S <= MAX_S)

@@ -120,8 +120,11 @@ struct __align__(16) Smem {
         Ring r;
         uint32_t stage[TILE_PIX][MAX_LEV];  // setup only: tuples proposed by the warps' group leaders
     } u;
-    float acc[2][MAX_SLOTS * BATCH];
-    float accZ[2][BATCH];
+    // per (slot, record) sums of a batch, triple-buffered: batch i accumulates into buffer i % 3,
+    // which is flushed after the batch's barrier; buffer (i+2) % 3 is zeroed meanwhile, so a
+    // single barrier per batch separates every write from every read
+    float acc[3][MAX_SLOTS * BATCH];
+    float accZ[3][BATCH];
     uint32_t slot_key[MAX_SLOTS][MAX_LEV];  // region id tuple of each slot
     uint32_t slot_atom[MAX_SLOTS][MAX_S];   // per slot: nlev codes of S slots each
     float slot_coef[MAX_SLOTS][MAX_S];
@@ -191,8 +194,8 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     }
     if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; }
     if (t < MAX_SLOTS) sm.slot_key[t][0] = SLOT_EMPTY;
-    for (int i = t; i < 2 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
-    if (t < 2 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
+    for (int i = t; i < 3 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
+    if (t < 3 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
     unsigned grp = FULL;
 #pragma unroll
     for (int l = 0; l < MAX_LEV; l++)
@@ -416,7 +419,10 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                     if (zsum != 0.f) atomicAdd(&sm.accZ[buf][lane], zsum);
                 }
             }
-            __syncthreads();  // B1
+        }
+        // B: the batch's sums are complete; also the termination vote (all pixels finished)
+        const int alive = __syncthreads_count(T > 0.f);
+        if (!overflow) {
             // ---- flush: nlev*S reds per (slot, Gaussian) into W_level, one per Gaussian into Z
             const int nitems = nslot * BATCH * LS;
             for (int i = t; i < nitems; i += TILE_PIX) {
@@ -443,14 +449,17 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const float z = sm.accZ[buf][t];
                 if (z > 0.f) atomicAdd(p.Z + __float_as_uint(q2[q_head + t].z), z);
             }
-            // zero the other accumulator buffer (flushed one batch ago)
-            for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[buf ^ 1][i] = 0.f;
-            if (t < BATCH) sm.accZ[buf ^ 1][t] = 0.f;
+            // zero the buffer of batch i+2 (flushed in batch i-1, before this batch's barrier)
+            const int bz = buf == 0 ? 2 : buf - 1;
+            for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[bz][i] = 0.f;
+            if (t < BATCH) sm.accZ[bz][t] = 0.f;
         }
+        // (no second barrier: the next refill writes only ring slots past this batch, and the
+        // next batch accumulates into another buffer)
         q_head = (q_head + n) & (QCAP - 1);
         q_count -= n;
-        buf ^= 1;
-        if (__syncthreads_count(T > 0.f) == 0) break;  // B2
+        buf = buf == 2 ? 0 : buf + 1;
+        if (alive == 0) break;
     }
 
     // carry the per-pixel state to the next chunk
