@@ -68,7 +68,9 @@ typedef struct {
 /* Counters accumulated since init / the last reset (read by scoup_uplift_get_stats). */
 typedef struct {
     int64_t views;          /* views added */
-    int64_t contributions;  /* fragments (v,p,i) with e > 0: terms of Eq. 5's sum */
+    int64_t contributions;  /* fragments (v,p,i) with e > 0: terms of Eq. 5's sum; counted
+                               while scoup_uplift_set_counters(h, 1) is on or for calls given a
+                               contributions_out array */
     int64_t tile_entries;   /* (Gaussian, tile) pairs binned */
     int64_t visible;        /* sum over views of Gaussians passing the projection culls */
     int64_t support_tests;  /* (pixel, Gaussian) pairs inside the Gaussian's square support
@@ -191,9 +193,9 @@ scoup_status scoup_uplift_get_accumulators(scoup_uplift *h, float **W, float **Z
 /* Copy the counters (synchronises the stream; returns latched EDATA if any). */
 scoup_status scoup_uplift_get_stats(scoup_uplift *h, scoup_stats *out);
 
-/* Enable (1) / disable (0) counting of support tests (scoup_stats.support_tests) in the
- * fused kernel; a slower instrumented variant, off by default.  Contributions are always
- * counted. */
+/* Enable (1) / disable (0) the instrumented fused kernel, which counts contributions and support
+ * tests (scoup_stats); off by default (the production kernel keeps no counters).  A call to
+ * add_views with a contributions_out array always uses the instrumented kernel. */
 scoup_status scoup_uplift_set_counters(scoup_uplift *h, int enable);
 
 /* Enable (1) / disable (0) per-kernel-class event timing; enabling clears the totals. */

@@ -164,7 +164,7 @@ struct scoup_uplift {
     double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
     double near_frac = 0.05;             // near chunk: this fraction of each view's visible Gaussians
     int bin_shift = 6;                  // bins of 2^bin_shift px squares
-    bool count_tests = false;           // raster counts support tests (scoup_uplift_set_counters)
+    bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
 };
 
 namespace {
@@ -514,7 +514,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.Tstate = b.Tstate;
     p.tile_live = b.tile_live;
     p.chunk = chunk;
-    p.count_tests = h->count_tests;
+    p.count_tests = h->count_tests || a.contrib_out != nullptr;
     p.nlev = h->nlev;
     for (int v = 0; v < c.nv; v++) {
         const int u = c.v0 + v;

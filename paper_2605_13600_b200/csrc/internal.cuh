@@ -303,7 +303,7 @@ struct RasterParams {
     float* Tstate;                // [nviews * H*W] transmittance carried between chunks
     uint8_t* tile_live;           // [nviews * tiles]
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate
-    bool count_tests;             // count support tests (slower variant; scoup_uplift_set_counters)
+    bool count_tests;             // instrumented variant: count contributions and support tests
     int nlev;                            // semantic levels fused in this pass (1..MAX_LEV)
     const uint32_t* region_ids[MAX_VB][MAX_LEV];  // [H*W] per view and level
     int64_t code_row0[MAX_VB][MAX_LEV];  // first row of (view, level) in the combined code table

@@ -6,7 +6,8 @@
 // candidate list of the bin that contains it (bins are power-of-two squares of pixels,
 // DESIGN.md §5) and walks it front to back:
 //
-//  refill   256 candidates at a time are tested against the tile (support box and the ellipse
+//  refill   256 candidates at a time (their records fetched one round ahead with cp.async into
+//           a per-thread staging slot) are tested against the tile (support box and the ellipse
 //           band spans, conservatively, band_relevant) and stably compacted into a shared-memory
 //           ring of records, so the ring stays in (depth, index) order;
 //  batch    32 ring records at a time: each warp ballots the records that may touch its 8x4 block
@@ -87,6 +88,14 @@ __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool 
     return v[0];
 }
 
+// cp.async of 16 bytes (zero-filled when !pred) and group completion.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // Fallback aggregation of one fragment: every level's code of the pixel (row < 0: unassigned at
 // that level, no W), and Z.  Scalars only, so the call needs no local-memory copies.
 __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* atoms, const float* coefs, int S,
@@ -125,6 +134,9 @@ struct __align__(16) Smem {
     // single barrier per batch separates every write from every read
     float acc[3][MAX_SLOTS * BATCH];
     float accZ[3][BATCH];
+    // candidate records of the next refill round, fetched with cp.async one round ahead (slot t
+    // is written and read by thread t only)
+    float4 st0[TILE_PIX], st1[TILE_PIX], st2[TILE_PIX], st3[TILE_PIX];
     uint32_t slot_key[MAX_SLOTS][MAX_LEV];  // region id tuple of each slot
     uint32_t slot_atom[MAX_SLOTS][MAX_S];   // per slot: nlev codes of S slots each
     float slot_coef[MAX_SLOTS][MAX_S];
@@ -142,9 +154,12 @@ struct __align__(16) Smem {
 #endif
 // NLEV1: a single semantic level (the BASELINE configs' default), so that every level loop and
 // the tuple bookkeeping fold away; else 1..MAX_LEV levels from p.nlev.
-template <bool COUNT_TESTS, bool NLEV1>
+// COUNT: the instrumented variant that also counts contributions and support tests (stats,
+// contributions_out); the production variant skips both counters in the pixel loop.
+template <bool COUNT, bool NLEV1>
 __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_kernel(const RasterParams p) {
-    __shared__ Smem sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
     const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
@@ -279,23 +294,35 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int L = p.L;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
+    // software-pipelined candidate fetch: the records of round k+1 are in flight (cp.async)
+    // while round k's batches are evaluated; the list indices are loaded one round further ahead
+    auto prefetch = [&](uint32_t e, bool ok) {
+        const uint32_t es = ok ? e : 0u;
+        cp_async16(&sm.st0[t], p.rec0 + es, ok);
+        cp_async16(&sm.st1[t], p.rec1 + es, ok);
+        cp_async16(&sm.st2[t], p.rec2 + es, ok);
+        cp_async16(&sm.st3[t], p.rec3 + es, ok);
+        cp_async_commit();
+    };
     uint32_t cursor = range.x;
+    {
+        const bool ok = cursor + t < range.y;
+        prefetch(ok ? __ldg(p.eval + cursor + t) : 0u, ok);
+    }
+    uint32_t e_next = cursor + TILE_PIX + t < range.y ? __ldg(p.eval + cursor + TILE_PIX + t) : 0u;
     uint32_t q_head = 0, q_count = 0;
     int buf = 0;
     while (true) {
         // ---- refill the ring: candidates with their warp masks (stable compaction)
         while (q_count < (uint32_t)BATCH && cursor < range.y) {
             const uint32_t idx = cursor + t;
-            bool acc = false;
-            float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
-            float4 r2 = make_float4(-1.f, -1.f, 0.f, 0.f), r3 = make_float4(0.f, 0.f, 0.f, -1.f);
-            if (idx < range.y) {
-                const uint32_t e = __ldg(p.eval + idx);  // chunk index of the Gaussian
-                r0 = __ldg(p.rec0 + e);
-                r2 = __ldg(p.rec2 + e);
-                r3 = __ldg(p.rec3 + e);
-                acc = band_relevant(r0, r2, r3, TX0, TX1, TY0, TY1);
-                if (acc) r1 = __ldg(p.rec1 + e);
+            cp_async_wait_all();  // this round's records (my staging slot)
+            const float4 r0 = sm.st0[t], r1 = sm.st1[t], r2 = sm.st2[t], r3 = sm.st3[t];
+            const bool acc = idx < range.y && band_relevant(r0, r2, r3, TX0, TX1, TY0, TY1);
+            {   // start the next round's fetch (my slot is free again)
+                const uint32_t nidx = cursor + TILE_PIX + t;
+                prefetch(e_next, nidx < range.y);
+                e_next = nidx + TILE_PIX < range.y ? __ldg(p.eval + nidx + TILE_PIX) : 0u;
             }
             const unsigned bal = __ballot_sync(FULL, acc);
             if (lane == 0) sm.wcnt[warp] = __popc(bal);
@@ -357,7 +384,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 // (a finished pixel, T == 0, needs no test of its own: its Tn = 0 < 1e-4 makes
                 // every later fragment a non-contributing stop that leaves T = 0)
                 const bool sq = ((mask >> j) & 1u) && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
-                const bool active = COUNT_TESTS && T > 0.f;
+                const bool active = COUNT && T > 0.f;
                 const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
                                           __fmul_rn(__fmul_rn(b.z, dy), dy));
                 const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
@@ -366,12 +393,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const bool con = pass && !(Tn < K_TMIN);
                 e[j] = con ? __fmul_rn(al, T) : 0.f;
                 T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
-                if (con) cbits |= 1u << j;
-                if (COUNT_TESTS && sq && active) tbits |= 1u << j;
+                if (COUNT && con) cbits |= 1u << j;
+                if (COUNT && sq && active) tbits |= 1u << j;
             }
         }
         }
-        const bool any = cbits != 0u;
+        // (uncounted: the reductions run whenever the warp evaluated a record; all-zero sums add
+        // nothing)
+        const bool any = COUNT ? cbits != 0u : mask != 0u;
         cnt += __popc(cbits);
         tests += __popc(tbits);
         if (overflow && any) {
@@ -462,15 +491,17 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         if (alive == 0) break;
     }
 
+    cp_async_wait_all();  // no copy may land in shared memory after the CTA retires
+
     // carry the per-pixel state to the next chunk
     if (inside) *Tpix = T;
     const int live = __syncthreads_count(T > 0.f);
     if (t == 0) p.tile_live[gtile] = live > 0 ? 1 : 0;
 
     // contributions (terms of Eq. 5's sum) and support tests
-    const unsigned c = __reduce_add_sync(FULL, cnt);
+    const unsigned c = COUNT ? __reduce_add_sync(FULL, cnt) : 0u;
     if (lane == 0 && c) atomicAdd(&sm.contrib, (unsigned long long)c);
-    if (COUNT_TESTS) {
+    if (COUNT) {
         const unsigned ts = __reduce_add_sync(FULL, tests);
         if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
     }
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             atomicAdd(p.contrib_ctr, sm.contrib);
             if (p.contrib_out[view]) atomicAdd(reinterpret_cast<unsigned long long*>(p.contrib_out[view]), sm.contrib);
         }
-        if (COUNT_TESTS && sm.tests) atomicAdd(p.support_ctr, sm.tests);
+        if (COUNT && sm.tests) atomicAdd(p.support_ctr, sm.tests);
     }
 }
 
@@ -489,17 +520,30 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (ntiles <= 0) return;
-    static_assert(sizeof(Smem) <= 48 * 1024, "raster smem must fit the static 48 KB window");
+    static_assert(sizeof(Smem) <= 3 * 1024 * 74, "three CTAs per SM must fit the 227 KB shared memory");
+    static bool attr_set = false;  // the opt-in above 48 KB of dynamic shared memory, once
+    if (!attr_set) {
+        cudaFuncSetAttribute(raster_aggregate_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem));
+        cudaFuncSetAttribute(raster_aggregate_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem));
+        cudaFuncSetAttribute(raster_aggregate_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem));
+        cudaFuncSetAttribute(raster_aggregate_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem));
+        attr_set = true;
+    }
+    const size_t smem = sizeof(Smem);
     if (p.nlev == 1) {
         if (p.count_tests)
-            raster_aggregate_kernel<true, true><<<ntiles, TILE_PIX, 0, s>>>(p);
+            raster_aggregate_kernel<true, true><<<ntiles, TILE_PIX, smem, s>>>(p);
         else
-            raster_aggregate_kernel<false, true><<<ntiles, TILE_PIX, 0, s>>>(p);
+            raster_aggregate_kernel<false, true><<<ntiles, TILE_PIX, smem, s>>>(p);
     } else {
         if (p.count_tests)
-            raster_aggregate_kernel<true, false><<<ntiles, TILE_PIX, 0, s>>>(p);
+            raster_aggregate_kernel<true, false><<<ntiles, TILE_PIX, smem, s>>>(p);
         else
-            raster_aggregate_kernel<false, false><<<ntiles, TILE_PIX, 0, s>>>(p);
+            raster_aggregate_kernel<false, false><<<ntiles, TILE_PIX, smem, s>>>(p);
     }
 }
 
