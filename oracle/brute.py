@@ -22,8 +22,8 @@ K_TMIN = f32(float.fromhex("0x1.a36e2ep-14"))
 K_HALF_LOG2E = f32(float.fromhex("-0x1.715476p-1"))
 K_LOG2E_NEG = f32(float.fromhex("-0x1.715476p+0"))
 _POLY = [f32(float.fromhex(h)) for h in
-         ["0x1.4258dap-13", "0x1.5f44dep-10", "0x1.3b2cc4p-7", "0x1.c6aed6p-5",
-          "0x1.ebfbdcp-3", "0x1.62e430p-1", "0x1p0"]]
+         ["0x1.5bba14p-10", "0x1.3cea88p-7", "0x1.c6b752p-5", "0x1.ebf9bcp-3",
+          "0x1.62e42ap-1", "0x1p0"]]
 
 
 def fma32(a, b, c):

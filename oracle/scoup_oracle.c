@@ -59,20 +59,19 @@ static const float K_HALF_LOG2E = -0x1.715476p-1f; /* -0.5*log2(e) */
 static const float K_LOG2E_NEG = -0x1.715476p+0f;  /* -log2(e) (= 2*K_HALF_LOG2E exactly) */
 
 /* exp2 specification, y <= 0 (DESIGN.md §3 "exp2_spec").
- * 2^y = 2^k * 2^f with k = round-half-even(y), f = y - k in [-1/2, 1/2]; 2^f by a degree-6
- * polynomial (Horner, explicit fmaf); 2^k applied exactly.  Max rel. error ~1e-7. */
+ * 2^y = 2^k * 2^f with k = round-half-even(y), f = y - k in [-1/2, 1/2]; 2^f by a degree-5 minimax
+ * polynomial (Horner, explicit fmaf); 2^k applied exactly.  Max rel. error 1.7e-7. */
 float ora_exp2_spec(float y) {
     if (y < -64.0f) return 0.0f;
     const float magic = 0x1.8p23f;
     float t = y + magic;        /* rounds y to the nearest integer, ties to even */
     float kf = t - magic;       /* exact */
     float f = y - kf;           /* exact (Sterbenz) */
-    float p = 0x1.4258dap-13f;
-    p = fmaf(p, f, 0x1.5f44dep-10f);
-    p = fmaf(p, f, 0x1.3b2cc4p-7f);
-    p = fmaf(p, f, 0x1.c6aed6p-5f);
-    p = fmaf(p, f, 0x1.ebfbdcp-3f);
-    p = fmaf(p, f, 0x1.62e430p-1f);
+    float p = 0x1.5bba14p-10f;
+    p = fmaf(p, f, 0x1.3cea88p-7f);
+    p = fmaf(p, f, 0x1.c6b752p-5f);
+    p = fmaf(p, f, 0x1.ebf9bcp-3f);
+    p = fmaf(p, f, 0x1.62e42ap-1f);
     p = fmaf(p, f, 1.0f);
     return ldexpf(p, (int)kf);  /* exact: result is a normal float */
 }

@@ -49,12 +49,11 @@ __device__ __forceinline__ float exp2_spec(float y) {
     float t = __fadd_rn(y, magic);  // round-half-even to an integer
     float kf = __fsub_rn(t, magic);
     float f = __fsub_rn(y, kf);
-    float p = 0x1.4258dap-13f;
-    p = __fmaf_rn(p, f, 0x1.5f44dep-10f);
-    p = __fmaf_rn(p, f, 0x1.3b2cc4p-7f);
-    p = __fmaf_rn(p, f, 0x1.c6aed6p-5f);
-    p = __fmaf_rn(p, f, 0x1.ebfbdcp-3f);
-    p = __fmaf_rn(p, f, 0x1.62e430p-1f);
+    float p = 0x1.5bba14p-10f;
+    p = __fmaf_rn(p, f, 0x1.3cea88p-7f);
+    p = __fmaf_rn(p, f, 0x1.c6b752p-5f);
+    p = __fmaf_rn(p, f, 0x1.ebf9bcp-3f);
+    p = __fmaf_rn(p, f, 0x1.62e42ap-1f);
     p = __fmaf_rn(p, f, 1.0f);
     // ldexp(p, k): bits(t) << 23 == k << 23 (mod 2^32) for t = 1.5*2^23 + k
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
