@@ -40,7 +40,7 @@ extern "C" {
 #endif
 
 #define SCOUP_NONE 0xFFFFFFFFu  /* unassigned pixel / empty code slot */
-#define SCOUP_MAX_L 256         /* implementation limits (EUNSUPPORTED beyond) */
+#define SCOUP_MAX_L 1024        /* implementation limits (EUNSUPPORTED beyond) */
 #define SCOUP_MAX_K 32
 #define SCOUP_MAX_S 16          /* per call: num_levels * S <= SCOUP_MAX_S */
 #define SCOUP_MAX_LEVELS 4
@@ -138,6 +138,10 @@ scoup_status scoup_uplift_init_levels(int device, void *cuda_stream, int64_t num
  *               (rows = max_v code_row0[v] + num_regions[v]); SCOUP_NONE = empty slot;
  *               coefficients finite and >= 0.  A code with more than K filled slots is
  *               truncated to its K largest (Algorithm 1's per-pixel TopK).
+ *               code_atoms NULL: DENSE region features (the dense feature uplift of Eq. 3,
+ *               P:76-80, the baseline SCOUP replaces): S must equal L, code_coefs holds each
+ *               region's full L-vector (any finite values), slot s adds to W[i][s]; no
+ *               truncation.  W / Z then gives Eq. 3's f_i.
  *  contributions_out  optional device int64 [V]: per-view contribution counts are ADDED.
  *  Errors: EINVAL (null pointers, V < 0, S < 1, size mismatch, bad camera intrinsics),
  *  EDATA (camera rotation not orthonormal with det +1 within 1e-5), EUNSUPPORTED (S >

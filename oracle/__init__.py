@@ -155,16 +155,18 @@ def uplift_accumulate(g, cams: Sequence, region_maps: np.ndarray, code_atoms: np
     Z = np.zeros(G, dtype=np.float64) if Z is None else Z
     frags = np.zeros(V, dtype=np.int64)
     ids = np.ascontiguousarray(region_maps, dtype=np.uint32)
-    atoms = np.ascontiguousarray(code_atoms, dtype=np.uint32)
     coefs = _f32(code_coefs)
-    S = atoms.shape[1]
+    S = coefs.shape[1]
+    # code_atoms None: dense features (Eq. 3 baseline, S = L)
+    atoms = None if code_atoms is None else np.ascontiguousarray(code_atoms, dtype=np.uint32)
     row0 = np.ascontiguousarray(code_row0, dtype=np.int64)
     nreg = np.ascontiguousarray(num_regions, dtype=np.int32)
     err = np.zeros(1, dtype=np.int64)
     camarr = cameras_array(cams)
     rc = lib().ora_uplift_accumulate(G, _p(_f32(g.means)), _p(_f32(g.scales)), _p(_f32(g.rotations)),
                                      _p(_f32(g.opacities)), V, camarr, _p(ids), _p(row0), _p(nreg),
-                                     _p(atoms), _p(coefs), S, L, K, _p(W), _p(Z), _p(frags), _p(err))
+                                     None if atoms is None else _p(atoms), _p(coefs), S, L, K, _p(W), _p(Z),
+                                     _p(frags), _p(err))
     if rc != 0:
         raise OracleError(rc, int(err[0]))
     return W, Z, frags

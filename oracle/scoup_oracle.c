@@ -343,15 +343,21 @@ int ora_uplift_accumulate(int64_t G, const float *means, const float *scales, co
         /* validate + truncate this view's codes (copy) */
         uint32_t *atoms = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(R > 0 ? R : 1) * S);
         float *coefs = (float *)malloc(sizeof(float) * (size_t)(R > 0 ? R : 1) * S);
+        /* code_atoms == NULL: dense region features F_v(p) in R^L (Eq. 3, the dense
+           uplift baseline): slot s is atom s, any finite value, no TopK truncation */
+        const int dense = code_atoms == NULL;
+        if (dense && S != L) { free(atoms); free(coefs); return -1; }
         for (int64_t j = 0; j < (int64_t)R * S; j++) {
             int64_t src = code_row0[v] * S + j;
-            atoms[j] = code_atoms[src];
+            atoms[j] = dense ? (uint32_t)(j % S) : code_atoms[src];
             coefs[j] = code_coefs[src];
-            if (atoms[j] != ORA_NONE && (atoms[j] >= (uint32_t)L || !isfinite(coefs[j]) || coefs[j] < 0.0f)) {
+            if (atoms[j] != ORA_NONE &&
+                (atoms[j] >= (uint32_t)L || !isfinite(coefs[j]) || (!dense && coefs[j] < 0.0f))) {
                 *err_index = src; free(atoms); free(coefs); return -4;
             }
         }
-        for (int32_t r = 0; r < R; r++) truncate_code(atoms + (int64_t)r * S, coefs + (int64_t)r * S, S, K);
+        if (!dense)
+            for (int32_t r = 0; r < R; r++) truncate_code(atoms + (int64_t)r * S, coefs + (int64_t)r * S, S, K);
         ora_proj *proj = (ora_proj *)calloc((size_t)(G > 0 ? G : 1), sizeof(ora_proj));
         float *T = (float *)malloc(sizeof(float) * (size_t)npx);
         unsigned char *done = (unsigned char *)malloc((size_t)npx);

@@ -366,6 +366,7 @@ struct CallArgs {
     int S;
     long long* contrib_out;
     int64_t npx;
+    bool dense;
 };
 
 // Depth pass of a batch: codes, per-view histogram (-> host), camera copy for the predicates.
@@ -515,6 +516,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.tile_live = b.tile_live;
     p.chunk = chunk;
     p.count_tests = h->count_tests || a.contrib_out != nullptr;
+    p.dense = a.dense;
     p.nlev = h->nlev;
     for (int v = 0; v < c.nv; v++) {
         const int u = c.v0 + v;
@@ -744,11 +746,19 @@ scoup_status scoup_uplift_add_views_levels(scoup_uplift* h, int32_t num_views, c
     const int nlev = h->nlev;
     if (!cameras || !region_ids || !code_row0 || !num_regions || !code_atoms || !code_coefs)
         return fail(SCOUP_EINVAL, "NULL argument");
-    for (int l = 0; l < nlev; l++)
-        if (!region_ids[l] || !code_atoms[l] || !code_coefs[l]) return fail(SCOUP_EINVAL, "NULL level argument");
+    // code_atoms[l] == NULL for every level: dense region features (Eq. 3 baseline), S == L
+    const bool dense = code_atoms[0] == nullptr;
+    for (int l = 0; l < nlev; l++) {
+        if (!region_ids[l] || !code_coefs[l]) return fail(SCOUP_EINVAL, "NULL level argument");
+        if ((code_atoms[l] == nullptr) != dense) return fail(SCOUP_EINVAL, "code_atoms NULL for some levels only");
+    }
     if (S < 1) return fail(SCOUP_EINVAL, "S < 1");
-    if (S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "S > SCOUP_MAX_S");
-    if (nlev * S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "num_levels * S > SCOUP_MAX_S");
+    if (dense) {
+        if (S != h->L) return fail(SCOUP_EINVAL, "dense features need S == L");
+    } else {
+        if (S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "S > SCOUP_MAX_S");
+        if (nlev * S > SCOUP_MAX_S) return fail(SCOUP_EUNSUPPORTED, "num_levels * S > SCOUP_MAX_S");
+    }
     const int Wd = cameras[0].width, Hd = cameras[0].height;
     std::vector<int64_t> rows(nlev, 0), loff(nlev, 0);
     for (int v = 0; v < num_views; v++) {
@@ -803,13 +813,17 @@ scoup_status scoup_uplift_add_views_levels(scoup_uplift* h, int32_t num_views, c
             }
             for (int l = 0; l < nlev; l++) {
                 if (rows[l] == 0) continue;
-                CK(cudaMemcpyAsync(h->code_atoms_in + loff[l] * S, code_atoms[l], sizeof(uint32_t) * rows[l] * S,
-                                   cudaMemcpyDefault, h->stream));
+                if (!dense)
+                    CK(cudaMemcpyAsync(h->code_atoms_in + loff[l] * S, code_atoms[l], sizeof(uint32_t) * rows[l] * S,
+                                       cudaMemcpyDefault, h->stream));
                 CK(cudaMemcpyAsync(h->code_coefs_in + loff[l] * S, code_coefs[l], sizeof(float) * rows[l] * S,
                                    cudaMemcpyDefault, h->stream));
             }
-            launch_ingest_codes(h->code_atoms_in, h->code_coefs_in, total_rows, S, h->K, h->L, h->code_atoms,
-                                h->code_coefs, latch_of(h), h->stream);
+            if (dense)
+                launch_ingest_dense(h->code_coefs_in, total_rows * S, h->code_coefs, latch_of(h), h->stream);
+            else
+                launch_ingest_codes(h->code_atoms_in, h->code_coefs_in, total_rows, S, h->K, h->L, h->code_atoms,
+                                    h->code_coefs, latch_of(h), h->stream);
         }
         bool ids_on_device = true;
         for (int l = 0; l < nlev; l++) ids_on_device = ids_on_device && is_device_ptr(region_ids[l]);
@@ -825,7 +839,8 @@ scoup_status scoup_uplift_add_views_levels(scoup_uplift* h, int32_t num_views, c
             CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
             ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
         }
-        CallArgs args{cams.data(), bn, row0c.data(), num_regions, num_views, S, (long long*)contributions_out, npx};
+        CallArgs args{cams.data(), bn, row0c.data(), num_regions, num_views, S, (long long*)contributions_out, npx,
+                      dense};
         int next = 0;  // first view not yet assigned to a batch
         auto start_batch = [&](Ctx& c) {
             int B = std::min(Bmax, num_views - next);

@@ -286,6 +286,7 @@ void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int k
 void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s);
 void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
                       const Binning& bn, uint8_t* flags, cudaStream_t s);
+void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s);
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K,
                          int L, uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s);
 
@@ -304,6 +305,7 @@ struct RasterParams {
     uint8_t* tile_live;           // [nviews * tiles]
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate
     bool count_tests;             // instrumented variant: count contributions and support tests
+    bool dense;                   // dense features (Eq. 3 baseline): S == L, atom = slot, no atoms table
     int nlev;                            // semantic levels fused in this pass (1..MAX_LEV)
     const uint32_t* region_ids[MAX_VB][MAX_LEV];  // [H*W] per view and level
     int64_t code_row0[MAX_VB][MAX_LEV];  // first row of (view, level) in the combined code table

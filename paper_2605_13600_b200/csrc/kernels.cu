@@ -464,6 +464,19 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t E, uint
     if (k == E - 1 || keys[k + 1] != key) ranges[key].y = (uint32_t)(k + 1);
 }
 
+// ------------------------------------------------------------------ ingest dense features
+// Dense region features (Eq. 3, the dense-uplift baseline): copy, finite check only.
+__global__ void ingest_dense_kernel(const float* __restrict__ in, int64_t n, float* __restrict__ out, ErrorLatch err) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    float v = in[k];
+    if (!isfinite(v)) {
+        latch_error(err, ERR_CODE, k);
+        v = 0.f;
+    }
+    out[k] = v;
+}
+
 // ------------------------------------------------------------------ ingest codes
 // Validate each region code and truncate it to its K largest slots (ties -> lower atom),
 // Algorithm 1's per-pixel TopK(W_v(p)).  No renormalisation.
@@ -679,6 +692,11 @@ void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int k
 void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s) {
     if (E <= 0) return;
     ranges_kernel<<<grid_for(E, 256), 256, 0, s>>>(keys_sorted, E, sentinel, ranges);
+}
+
+void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s) {
+    if (n <= 0) return;
+    ingest_dense_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, out, err);
 }
 
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K, int L,

@@ -106,7 +106,7 @@ __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* a
         if (row < 0) continue;
         float* Wl = W + (int64_t)l * level_stride;
         for (int s = 0; s < S; s++) {
-            const uint32_t at = __ldg(atoms + row + s);
+            const uint32_t at = atoms ? __ldg(atoms + row + s) : (uint32_t)s;  // (no atoms: dense)
             if (at != NONE) atomicAdd(Wl + (int64_t)g * L + at, __fmul_rn(__ldg(coefs + row + s), ev));
         }
     }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int LS = nlev * S;  // W updates per (slot, Gaussian): every level's code
     const int ls_log2 = (LS & (LS - 1)) == 0 ? __ffs(LS) - 1 : -1;
     const int s_log2 = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
-    for (int i = t; i < nslot * LS; i += TILE_PIX) {
+    for (int i = t; i < (p.dense ? 0 : nslot * LS); i += TILE_PIX) {  // (dense: read in the flush)
         const int q = i / LS, ls = i - q * LS, l = ls / S, s = ls - l * S;
         const uint32_t k = sm.slot_key[q][l];
         uint32_t a = NONE;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                         rw[l] = (k != NONE && k < (uint32_t)p.num_regions[view][l])
                                     ? (p.code_row0[view][l] + (int64_t)k) * S : -1;
                     }
-                    overflow_reds(p.W, p.Z, p.code_atoms, p.code_coefs, S, L, nlev, p.W_level_stride,
+                    overflow_reds(p.W, p.Z, p.dense ? nullptr : p.code_atoms, p.code_coefs, S, L, nlev, p.W_level_stride,
                                   __float_as_uint(q2[q_head + j].z), e[j], rw[0], rw[1], rw[2], rw[3]);
                 }
             }
@@ -466,12 +466,22 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                     ls = rem - j * LS;
                 }
                 const float v = sm.acc[buf][q * BATCH + j];
-                const uint32_t a = sm.slot_atom[q][ls];
-                if (v > 0.f && a != NONE) {
-                    const int l = s_log2 >= 0 ? ls >> s_log2 : ls / S;
-                    atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
-                              __fmul_rn(sm.slot_coef[q][ls], v));
+                const int l = s_log2 >= 0 ? ls >> s_log2 : ls / S;
+                uint32_t a;
+                float c;
+                if (p.dense) {  // dense features (Eq. 3 baseline): slot s is atom s, from the table
+                    a = (uint32_t)(ls - l * S);
+                    const uint32_t k = sm.slot_key[q][l];
+                    c = k != KEY_NONE && v > 0.f ? __ldg(p.code_coefs + (p.code_row0[view][l] + (int64_t)k) * S + a)
+                                                 : 0.f;
+                    if (k == KEY_NONE) a = NONE;
+                } else {
+                    a = sm.slot_atom[q][ls];
+                    c = sm.slot_coef[q][ls];
                 }
+                if (v > 0.f && a != NONE)
+                    atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
+                              __fmul_rn(c, v));
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];

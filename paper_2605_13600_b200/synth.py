@@ -297,6 +297,23 @@ def make_codes(cfg: SceneConfig, level: int = 0, seed: int = 0,
                  np.full(len(views), R, dtype=np.int32))
 
 
+def make_dense_features(cfg: SceneConfig, D: int, level: int = 0, seed: int = 0,
+                        views: Optional[Sequence[int]] = None) -> Codes:
+    """Dense per-(view, region) features in R^D (unit-norm normal vectors, CLIP-like), for the
+    dense feature uplift of Eq. 3, the baseline sparse codes replace.
+    Returned as Codes with atoms=None (S = D slots, slot s = feature dimension s)."""
+    views = list(range(cfg.num_views)) if views is None else list(views)
+    R = cfg.regions[level]
+    out = []
+    for v in views:
+        rng = _rng(seed, 5, v, level)
+        f = rng.normal(size=(R, D))
+        f /= np.linalg.norm(f, axis=1, keepdims=True)
+        out.append(f.astype(np.float32))
+    row0 = np.arange(len(views), dtype=np.int64) * R
+    return Codes(None, np.concatenate(out), row0, np.full(len(views), R, dtype=np.int32))
+
+
 def make_region_maps_numpy(cfg: SceneConfig, level: int = 0, seed: int = 0,
                            views: Optional[Sequence[int]] = None) -> np.ndarray:
     views = list(range(cfg.num_views)) if views is None else list(views)

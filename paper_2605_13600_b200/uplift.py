@@ -56,20 +56,20 @@ class SparseUplift:
         """region_ids: [V,H,W] uint32 numpy (host) or int32/uint32 torch tensor (device or host).
         codes: synth.Codes-like (atoms [rows,S] u32, coefs [rows,S] f32, row0 [V], num_regions [V]).
         With levels > 1: a sequence of per-level region maps and a sequence of per-level codes."""
-        def prep(c):
+        def prep(c):  # c.atoms None: dense region features (Eq. 3 baseline), S == L
             atoms = c.atoms if not isinstance(c.atoms, np.ndarray) else np.ascontiguousarray(c.atoms, np.uint32)
             coefs = c.coefs if not isinstance(c.coefs, np.ndarray) else np.ascontiguousarray(c.coefs, np.float32)
             return atoms, coefs
         if self.levels == 1:
             atoms, coefs = prep(codes)
-            S = int(atoms.shape[1])
+            S = int(coefs.shape[1])
             abi.scoup_uplift_add_views(self._h, list(cameras), region_ids, codes.row0, codes.num_regions,
                                        atoms, coefs, S, contributions_out)
             return
         if len(region_ids) != self.levels or len(codes) != self.levels:
             raise ValueError(f"expected {self.levels} region maps and code tables")
         pc = [prep(c) for c in codes]
-        S = int(pc[0][0].shape[1])
+        S = int(pc[0][1].shape[1])
         row0 = np.stack([np.asarray(c.row0, np.int64) for c in codes])
         nreg = np.stack([np.asarray(c.num_regions, np.int32) for c in codes])
         abi.scoup_uplift_add_views_levels(self._h, list(cameras), list(region_ids), row0, nreg,

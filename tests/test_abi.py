@@ -66,7 +66,7 @@ def test_host_side_validation_without_gpu(lib):
     assert L.scoup_uplift_init(0, None, 0, None, None, None, None, 8, 0, None, None, 0, C.byref(h)) == 1
     assert L.scoup_uplift_init(0, None, -1, None, None, None, None, 8, 2, None, None, 0, C.byref(h)) == 1
     assert L.scoup_uplift_init(0, None, 10, None, None, None, None, 8, 2, None, None, 0, None) == 1
-    assert L.scoup_uplift_init(0, None, 0, None, None, None, None, 512, 2, None, None, 0, C.byref(h)) == 6
+    assert L.scoup_uplift_init(0, None, 0, None, None, None, None, 2048, 2, None, None, 0, C.byref(h)) == 6
     assert L.scoup_uplift_add_views(None, 1, None, None, None, None, None, None, 4, None) == 1
     assert L.scoup_uplift_finalize_topk(None, 0, 1, None, None, None, None) == 1
     L.scoup_uplift_free(None)  # no-op

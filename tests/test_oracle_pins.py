@@ -444,3 +444,44 @@ def test_oracle_errors():
     assert ei.value.code == -4
     with pytest.raises(oracle.OracleError):
         oracle.uplift(g, [cam], ids, full_frame_codes([[(1, 1.0)]]), 8, 9)
+
+
+def test_dense_feature_path(tiny_scene):
+    """Eq. 3, the dense-uplift baseline (code_atoms = None: every region carries a full
+    feature vector of L values, any sign): (a) S:301, a constant feature u gives W_i = u Z_i
+    exactly up to rounding; (b) decoded features F_v(r) = W_v(r) C accumulate to the same
+    sum over fragments as the fragment lists, which pins the dense path independently."""
+    cfg, scene, maps, codes = tiny_scene
+    cams = scene.cameras[:2]
+    g = scene.gaussians
+    rng = np.random.default_rng(12)
+    D = 24
+    u = rng.normal(size=D).astype(np.float32)
+    R = int(codes.num_regions[0])
+    feats = np.tile(u, (2 * R, 1))
+    row0 = np.array([0, R], np.int64)
+    nreg = np.array([R, R], np.int32)
+    W, Z, fr = oracle.uplift_accumulate(g, cams, maps[:2], None, feats, row0, nreg, D, 1)
+    seen = Z > 0
+    assert seen.sum() > 100
+    assert np.allclose(W[seen], np.outer(Z[seen], u.astype(np.float64)), rtol=1e-6, atol=1e-9)
+    # (b) decoded codes as dense features
+    C = rng.normal(size=(cfg.L, D))
+    Fr = np.zeros((2 * R, D), np.float32)
+    for v in range(2):
+        for r in range(R):
+            row = codes.row0[v] + r
+            w = np.zeros(cfg.L)
+            for a, c in zip(codes.atoms[row], codes.coefs[row]):
+                if a != NONE:
+                    w[a] += c
+            Fr[v * R + r] = (w @ C).astype(np.float32)
+    Wd, Zd, _ = oracle.uplift_accumulate(g, cams, maps[:2], None, Fr, row0, nreg, D, 1)
+    F = np.zeros((g.count, D))
+    for v, cam in enumerate(cams):
+        T, pix, gid, e = oracle.render_view(g, cam)
+        rid = maps[v].ravel()[pix].astype(np.int64)
+        prod = (Fr[v * R + rid] * e[:, None]).astype(np.float32)  # the spec's fp32 products c * e
+        np.add.at(F, gid, prod.astype(np.float64))
+    assert np.allclose(Wd, F, rtol=1e-9, atol=1e-12)
+    assert np.allclose(Z, Zd)
