@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dense", type=int, default=0,
+                    help="dense feature uplift baseline (Eq. 3) with D-dim region features instead of codes")
     return ap.parse_args()
 
 
@@ -205,6 +207,9 @@ def main():
         cfg = cfg.with_(num_views=args.views)
     scene = synth.make_scene(cfg, 0)
     g = scene.gaussians
+    dense = args.dense > 0
+    if dense:  # Eq. 3 baseline: D-dim features per region, one level, no Top-K (f_i = W_i / Z_i)
+        cfg = cfg.with_(L=args.dense, S=args.dense, regions=cfg.regions[:1])
     G, L, K = g.count, cfg.L, cfg.K
     from paper_2605_13600_b200 import distributed as D
     my_views = D.views_for_rank(cfg.num_views, rank, world)
@@ -212,9 +217,10 @@ def main():
     # semantic levels (configs[2]: three nested levels) are fused into one raster pass
     nlev = len(cfg.regions)
     maps_l = [synth.make_region_maps_torch(cfg, dev, level=l, seed=0, views=my_views) for l in range(nlev)]
-    codes_hl = [synth.make_codes(cfg, level=l, seed=0, views=my_views) for l in range(nlev)]
-    codes_l = [synth.Codes(torch.from_numpy(c.atoms.view(np.int32)).to(dev), torch.from_numpy(c.coefs).to(dev),
-                           c.row0, c.num_regions) for c in codes_hl]
+    codes_hl = [synth.make_dense_features(cfg, L, level=l, seed=0, views=my_views) if dense else
+                synth.make_codes(cfg, level=l, seed=0, views=my_views) for l in range(nlev)]
+    codes_l = [synth.Codes(None if c.atoms is None else torch.from_numpy(c.atoms.view(np.int32)).to(dev),
+                           torch.from_numpy(c.coefs).to(dev), c.row0, c.num_regions) for c in codes_hl]
     maps = maps_l[0]
     gd = synth.Gaussians(*[torch.from_numpy(a).to(dev) for a in (g.means, g.scales, g.rotations, g.opacities)])
     Npad = D.padded_rows(G, world)
@@ -230,6 +236,8 @@ def main():
             u.add_views(cams, m_l, c_l)
 
     def finalize_all(u, out_atoms=None, out_coefs=None):
+        if dense:  # Eq. 3 needs no Top-K: f_i = W_i / Z_i (W is the output)
+            return
         for lvl in range(nlev):
             if world > 1:
                 Wl = u.W if nlev == 1 else u.W[lvl]
@@ -317,7 +325,7 @@ def main():
         nrows = G if world == 1 else shard
         atoms_h = torch.empty((nrows, K), dtype=torch.int32).pin_memory()
         coefs_h = torch.empty((nrows, K), dtype=torch.float32).pin_memory()
-        codes_hpl = [synth.Codes(torch.from_numpy(c.atoms.view(np.int32)).pin_memory(),
+        codes_hpl = [synth.Codes(None if c.atoms is None else torch.from_numpy(c.atoms.view(np.int32)).pin_memory(),
                                  torch.from_numpy(c.coefs).pin_memory(), c.row0, c.num_regions) for c in codes_hl]
 
         def e2e_step():
@@ -337,8 +345,8 @@ def main():
         n_e2e = max(1, min(args.steps, 2))
         e2e_s = max_over_ranks((time.perf_counter() - t0) / n_e2e)
         h2d = sum_over_ranks(sum(m.numel() for m in maps_hl) * 4 + G * 44 +
-                             sum(c.atoms.numel() for c in codes_hpl) * 8)
-        d2h = sum_over_ranks(nlev * nrows * K * 8)
+                             sum(c.coefs.numel() * (4 if c.atoms is None else 8) for c in codes_hpl))
+        d2h = sum_over_ranks(0 if dense else nlev * nrows * K * 8)
         e2e = {"value": contrib_step / e2e_s, "unit": "contributions/s", "seconds_per_step": e2e_s,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
@@ -353,7 +361,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "scene_uplift_s": ms_per_step / 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "gaussians": G, "views": cfg.num_views, "width": cfg.width,
+            "config": {"workload": cfg.name + (f"-dense{L}" if dense else ""), "gaussians": G, "views": cfg.num_views, "width": cfg.width,
                        "height": cfg.height, "L": L, "S": cfg.S, "K": K, "levels": nlev,
                        "regions_per_view": list(cfg.regions),
                        "parallelism": f"view-sharded x{world} + reduce-scatter" if world > 1 else "single GPU",
