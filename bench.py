@@ -177,10 +177,11 @@ def run_reference(args):
     ms = statistics.median([r["seconds"] for r in per]) * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "contributions/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "gaussians": cfg.num_gaussians, "views": cfg.num_views,
-                       "width": cfg.width, "height": cfg.height, "L": cfg.L, "K": cfg.K,
-                       "step": "one view of the workload per step (bounded sample)"},
+                       "width": cfg.width, "height": cfg.height, "L": cfg.L, "S": cfg.S, "K": cfg.K,
+                       "levels": 1, "regions_per_view": list(cfg.regions[:1]), "parallelism": "CPU oracle, 1 thread",
+                       "step": "one view of the workload per step (bounded sample: middle third of its rows)"},
             "cpu_baseline": {"value": value, "unit": "contributions/s", "cores": 1, "kind": "oracle",
                              "sample": "per step the middle third of one view's rows (all Gaussians), views 0.."
                                        + str(args.warmup + args.steps - 1)},
