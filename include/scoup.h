@@ -181,6 +181,29 @@ scoup_status scoup_uplift_finalize_topk(scoup_uplift *h, int64_t first_row, int6
                                         const float *W_rows, const float *Z_rows,
                                         uint32_t *out_atoms, float *out_coefs);
 
+/*
+ * Sparse coefficient rendering (Eq. 7):
+ *   W_hat_v(p) = sum_{i in N_{v,p}} w_hat_i e_i(v,p)
+ * for each view, with the handle's Gaussians and the K-sparse codes w_hat_i (the output of
+ * scoup_uplift_finalize_topk: code_atoms [N,K] uint32 / code_coefs [N,K] float32, device;
+ * SCOUP_NONE slots ignored).  e_i(v,p) are the same fragment weights as the uplift's
+ * (bit-identical to the oracle's).  out: device float32 [V, H, W, L] (row-major, a dense
+ * L-vector per pixel), overwritten.  L <= 128.  Stream-ordered; accumulators untouched.
+ * Errors: EINVAL (NULL / host buffers, K out of range, camera problems as add_views), EDATA
+ * (non-rigid camera), EUNSUPPORTED (L > 128, image too large), ECUDA.
+ */
+scoup_status scoup_uplift_render_views(scoup_uplift *h, int32_t num_views, const scoup_camera *cameras,
+                                       const uint32_t *code_atoms, const float *code_coefs, int32_t K, float *out);
+
+/*
+ * Codebook decode (Eq. 8): F = W_hat C for num_pixels rendered coefficient
+ * vectors W_hat [P, L] (e.g. scoup_uplift_render_views' output) and a codebook C [L, D],
+ * all float32 row-major on the device; F [P, D] overwritten.  A plain library GEMM (cuBLAS
+ * SGEMM, fp32) on the handle's stream.  Errors: EINVAL, EUNSUPPORTED (P >= 2^31), ECUDA.
+ */
+scoup_status scoup_uplift_decode(scoup_uplift *h, int64_t num_pixels, const float *W_hat, const float *C, int32_t D,
+                                 float *F);
+
 /* scoup_uplift_finalize_topk on level `level` (0 .. num_levels-1) of a multi-level handle;
  * scoup_uplift_finalize_topk is level 0.  EINVAL for a level out of range. */
 scoup_status scoup_uplift_finalize_topk_level(scoup_uplift *h, int32_t level, int64_t first_row, int64_t num_rows,

@@ -45,6 +45,7 @@ class scoup_timing(C.Structure):
 
 EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
            "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
+           "scoup_uplift_render_views", "scoup_uplift_decode",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
            "scoup_uplift_free", "scoup_last_error", "scoup_version"]
@@ -64,6 +65,8 @@ def lib():
         L.scoup_uplift_init_levels.argtypes = [C.c_int, P, i64, P, P, P, P, i32, i32, i32, P, P, i64, C.POINTER(P)]
         L.scoup_uplift_add_views_levels.argtypes = [P, i32, P, P, P, P, P, P, i32, P]
         L.scoup_uplift_finalize_topk_level.argtypes = [P, i32, i64, i64, P, P, P, P]
+        L.scoup_uplift_render_views.argtypes = [P, i32, P, P, P, i32, P]
+        L.scoup_uplift_decode.argtypes = [P, i64, P, P, i32, P]
         L.scoup_uplift_add_views.argtypes = [P, i32, P, P, P, P, P, P, i32, P]
         L.scoup_uplift_finalize_topk.argtypes = [P, i64, i64, P, P, P, P]
         L.scoup_uplift_reset.argtypes = [P]
@@ -78,6 +81,8 @@ def lib():
         L.scoup_version.restype = C.c_char_p
         for name in ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
                      "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
+                     "scoup_uplift_render_views", "scoup_uplift_decode",
+           "scoup_uplift_render_views", "scoup_uplift_decode",
                      "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
                      "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
             getattr(L, name).restype = C.c_int
@@ -158,6 +163,15 @@ def scoup_uplift_finalize_topk_level(h: int, level: int, first_row: int, num_row
                                      out_coefs) -> None:
     _check(lib().scoup_uplift_finalize_topk_level(h, level, first_row, num_rows, ptr(W_rows), ptr(Z_rows),
                                                   ptr(out_atoms), ptr(out_coefs)))
+
+
+def scoup_uplift_render_views(h: int, cameras: Sequence, code_atoms, code_coefs, K: int, out) -> None:
+    _check(lib().scoup_uplift_render_views(h, len(cameras), cameras_struct(cameras), ptr(code_atoms), ptr(code_coefs),
+                                           K, ptr(out)))
+
+
+def scoup_uplift_decode(h: int, num_pixels: int, W_hat, C, D: int, F) -> None:
+    _check(lib().scoup_uplift_decode(h, num_pixels, ptr(W_hat), ptr(C), D, ptr(F)))
 
 
 def scoup_uplift_add_views(h: int, cameras: Sequence, region_ids, code_row0, num_regions, code_atoms,

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "kernels.cu", "raster.cu"]
+SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu"]
 HEADERS = ["internal.cuh"]
 LIB = os.path.join(HERE, "libscoup.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return LIB
     tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-lcublas"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -10,6 +10,7 @@
 // contexts on two streams are software-pipelined: while the host waits for view v's total,
 // the GPU runs view v-1's raster.
 // finalize_topk runs Eq. 6 on the requested rows.
+#include <cublas_v2.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
@@ -165,6 +166,7 @@ struct scoup_uplift {
     double near_frac = 0.05;             // near chunk: this fraction of each view's visible Gaussians
     int bin_shift = 6;                  // bins of 2^bin_shift px squares
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
+    cublasHandle_t blas = nullptr;      // decode GEMM (Eq. 8), created on first use
 };
 
 namespace {
@@ -367,6 +369,12 @@ struct CallArgs {
     long long* contrib_out;
     int64_t npx;
     bool dense;
+    // render (Eq. 7) instead of uplift
+    bool render = false;
+    const uint32_t* r_atoms = nullptr;
+    const float* r_coefs = nullptr;
+    int rK = 0;
+    float* r_out = nullptr;
 };
 
 // Depth pass of a batch: codes, per-view histogram (-> host), camera copy for the predicates.
@@ -517,10 +525,15 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.chunk = chunk;
     p.count_tests = h->count_tests || a.contrib_out != nullptr;
     p.dense = a.dense;
+    p.r_atoms = a.r_atoms;
+    p.r_coefs = a.r_coefs;
+    p.rK = a.rK;
+    p.r_out = a.r_out;
+    p.r_view0 = c.v0;
     p.nlev = h->nlev;
     for (int v = 0; v < c.nv; v++) {
         const int u = c.v0 + v;
-        for (int l = 0; l < h->nlev; l++) {
+        for (int l = 0; l < (a.render ? 0 : h->nlev); l++) {  // the render reads no region maps
             p.region_ids[v][l] = c.ids_dev[v][l];
             p.code_row0[v][l] = a.code_row0[(int64_t)l * a.V + u];
             p.num_regions[v][l] = a.num_regions[(int64_t)l * a.V + u];
@@ -539,7 +552,8 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.support_ctr = h->d_stats + 4;
     p.err = latch_of(h);
     ev_mark(c, mark0);
-    launch_raster(p, c.s);
+    if (a.render) launch_render(p, c.s);
+    else launch_raster(p, c.s);
     ev_mark(c, mark0 + 1);
     h->kernel_launches += 1;
     return SCOUP_OK;
@@ -582,6 +596,91 @@ scoup_status step_far_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
 }
 
 __global__ void add_u64(unsigned long long* p, unsigned long long v) { atomicAdd(p, v); }
+
+// The per-view pipeline shared by the uplift and the render: view batches through the two
+// contexts' step machines (depth pass, near chunk, near raster + far selection, far chunk, far
+// raster), joined back into the handle's stream.  region_ids: nlev per-level maps (uplift) or
+// none (render).
+scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* cameras, const Binning& bn,
+                       int64_t npx, CallArgs& args, const uint32_t* const* region_ids, int nlev) {
+    try {
+        bool ids_on_device = true;
+        for (int l = 0; l < nlev; l++) ids_on_device = ids_on_device && is_device_ptr(region_ids[l]);
+        std::vector<Camera> cams(num_views);
+        for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
+        // ---- view batches: up to MAX_VB views per pass (bounded by the bin table and by the
+        // depth-code width: view bits + code bits <= 32)
+        const int Bmax = std::max(1, std::min(MAX_VB, (int)num_views));
+        const int ntiles = bn.tiles_x * bn.tiles_y;
+        // ---- fork the two pipeline contexts off the caller's stream
+        CK(cudaEventRecord(h->ev_fork, h->stream));
+        for (int i = 0; i < 2; i++) {
+            CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
+            ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
+        }
+        args.cams = cams.data();
+        int next = 0;  // first view not yet assigned to a batch
+        auto start_batch = [&](Ctx& c) {
+            int B = std::min(Bmax, num_views - next);
+            int kb = 31;
+            for (;; B = std::max(1, B / 2)) {
+                int vbits = 0;
+                while ((1 << vbits) < B) vbits++;
+                kb = std::min(31, depth_key_bits(h, &cams[next], B));
+                if (kb + vbits <= 32 || B == 1) break;
+            }
+            c.v0 = next;
+            c.nv = B;
+            c.key_bits = kb;
+            next += B;
+            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx * nlev), c.s, 1.0);
+            for (int v = 0; v < c.nv; v++) {
+                const int u = c.v0 + v;
+                for (int l = 0; l < nlev; l++) {
+                    if (ids_on_device) {
+                        c.ids_dev[v][l] = region_ids[l] + (int64_t)u * npx;
+                    } else {
+                        uint32_t* dst = c.ids_stage + ((int64_t)l * Bmax + v) * npx;
+                        CK(cudaMemcpyAsync(dst, region_ids[l] + (int64_t)u * npx, sizeof(uint32_t) * npx,
+                                           cudaMemcpyHostToDevice, c.s));
+                        c.ids_dev[v][l] = dst;
+                    }
+                }
+            }
+            step_depth(h, c, args);
+        };
+        scoup_status st = SCOUP_OK;
+        for (int ci = 0; ci < 2; ci++) h->ctx[ci].step = ST_IDLE;
+        for (bool busy = true; busy && st == SCOUP_OK;) {
+            busy = false;
+            for (int ci = 0; ci < 2 && st == SCOUP_OK; ci++) {
+                Ctx& c = h->ctx[ci];
+                switch (c.step) {
+                    case ST_IDLE:
+                        if (next < num_views) { start_batch(c); busy = true; }
+                        break;
+                    case ST_NEAR_FRONT: step_near_front(h, c, args); busy = true; break;
+                    case ST_NEAR_RASTER: st = step_near_raster(h, c, args); busy = true; break;
+                    case ST_FAR_FRONT: step_far_front(h, c, args); busy = true; break;
+                    case ST_FAR_RASTER: st = step_far_raster(h, c, args); busy = true; break;
+                }
+            }
+        }
+        // ---- join back into the caller's stream
+        for (int i = 0; i < 2; i++) {
+            CK(cudaEventRecord(h->ev_join[i], h->ctx[i].s));
+            CK(cudaStreamWaitEvent(h->stream, h->ev_join[i], 0));
+        }
+        add_u64<<<1, 1, 0, h->stream>>>(h->d_stats + 0, (unsigned long long)num_views);
+        h->kernel_launches += 1;
+        CK(cudaGetLastError());
+        return st;
+    } catch (const CudaError& e) {
+        return fail(e.err == cudaErrorMemoryAllocation ? SCOUP_ENOMEM : SCOUP_ECUDA,
+                    std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+}
+
 
 }  // namespace
 
@@ -825,82 +924,83 @@ scoup_status scoup_uplift_add_views_levels(scoup_uplift* h, int32_t num_views, c
                 launch_ingest_codes(h->code_atoms_in, h->code_coefs_in, total_rows, S, h->K, h->L, h->code_atoms,
                                     h->code_coefs, latch_of(h), h->stream);
         }
-        bool ids_on_device = true;
-        for (int l = 0; l < nlev; l++) ids_on_device = ids_on_device && is_device_ptr(region_ids[l]);
-        std::vector<Camera> cams(num_views);
-        for (int v = 0; v < num_views; v++) cams[v] = to_cam(cameras[v]);
-        // ---- view batches: up to MAX_VB views per pass (bounded by the bin table and by the
-        // depth-code width: view bits + code bits <= 32)
-        const int Bmax = std::max(1, std::min(MAX_VB, (int)num_views));
-        const int ntiles = bn.tiles_x * bn.tiles_y;
-        // ---- fork the two pipeline contexts off the caller's stream
-        CK(cudaEventRecord(h->ev_fork, h->stream));
-        for (int i = 0; i < 2; i++) {
-            CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
-            ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
-        }
-        CallArgs args{cams.data(), bn, row0c.data(), num_regions, num_views, S, (long long*)contributions_out, npx,
+        CallArgs args{nullptr, bn, row0c.data(), num_regions, num_views, S, (long long*)contributions_out, npx,
                       dense};
-        int next = 0;  // first view not yet assigned to a batch
-        auto start_batch = [&](Ctx& c) {
-            int B = std::min(Bmax, num_views - next);
-            int kb = 31;
-            for (;; B = std::max(1, B / 2)) {
-                int vbits = 0;
-                while ((1 << vbits) < B) vbits++;
-                kb = std::min(31, depth_key_bits(h, &cams[next], B));
-                if (kb + vbits <= 32 || B == 1) break;
-            }
-            c.v0 = next;
-            c.nv = B;
-            c.key_bits = kb;
-            next += B;
-            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx * nlev), c.s, 1.0);
-            for (int v = 0; v < c.nv; v++) {
-                const int u = c.v0 + v;
-                for (int l = 0; l < nlev; l++) {
-                    if (ids_on_device) {
-                        c.ids_dev[v][l] = region_ids[l] + (int64_t)u * npx;
-                    } else {
-                        uint32_t* dst = c.ids_stage + ((int64_t)l * Bmax + v) * npx;
-                        CK(cudaMemcpyAsync(dst, region_ids[l] + (int64_t)u * npx, sizeof(uint32_t) * npx,
-                                           cudaMemcpyHostToDevice, c.s));
-                        c.ids_dev[v][l] = dst;
-                    }
-                }
-            }
-            step_depth(h, c, args);
-        };
-        scoup_status st = SCOUP_OK;
-        for (int ci = 0; ci < 2; ci++) h->ctx[ci].step = ST_IDLE;
-        for (bool busy = true; busy && st == SCOUP_OK;) {
-            busy = false;
-            for (int ci = 0; ci < 2 && st == SCOUP_OK; ci++) {
-                Ctx& c = h->ctx[ci];
-                switch (c.step) {
-                    case ST_IDLE:
-                        if (next < num_views) { start_batch(c); busy = true; }
-                        break;
-                    case ST_NEAR_FRONT: step_near_front(h, c, args); busy = true; break;
-                    case ST_NEAR_RASTER: st = step_near_raster(h, c, args); busy = true; break;
-                    case ST_FAR_FRONT: step_far_front(h, c, args); busy = true; break;
-                    case ST_FAR_RASTER: st = step_far_raster(h, c, args); busy = true; break;
-                }
-            }
-        }
-        // ---- join back into the caller's stream
-        for (int i = 0; i < 2; i++) {
-            CK(cudaEventRecord(h->ev_join[i], h->ctx[i].s));
-            CK(cudaStreamWaitEvent(h->stream, h->ev_join[i], 0));
-        }
-        add_u64<<<1, 1, 0, h->stream>>>(h->d_stats + 0, (unsigned long long)num_views);
-        h->kernel_launches += 1 + (total_rows > 0 ? 1 : 0);
-        CK(cudaGetLastError());
+        const scoup_status st = run_views(h, num_views, cameras, bn, npx, args, region_ids, nlev);
+        h->kernel_launches += total_rows > 0 ? 1 : 0;
         if (st != SCOUP_OK) return st;
     } catch (const CudaError& e) {
         return fail(e.err == cudaErrorMemoryAllocation ? SCOUP_ENOMEM : SCOUP_ECUDA,
                     std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
     }
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_render_views(scoup_uplift* h, int32_t num_views, const scoup_camera* cameras,
+                                       const uint32_t* code_atoms, const float* code_coefs, int32_t K, float* out) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (h->latched) return fail(SCOUP_ESTATE, "a latched data error is pending; call scoup_uplift_reset");
+    if (num_views < 0) return fail(SCOUP_EINVAL, "num_views < 0");
+    if (num_views == 0) return SCOUP_OK;
+    if (!cameras || !code_atoms || !code_coefs || !out) return fail(SCOUP_EINVAL, "NULL argument");
+    if (K < 1 || K > SCOUP_MAX_K) return fail(SCOUP_EINVAL, "K out of range");
+    if (h->L > 128) return fail(SCOUP_EUNSUPPORTED, "render needs L <= 128 (per-pixel rows in shared memory)");
+    if (!is_device_ptr(code_atoms) || !is_device_ptr(code_coefs) || !is_device_ptr(out))
+        return fail(SCOUP_EINVAL, "render buffers must be device memory");
+    const int Wd = cameras[0].width, Hd = cameras[0].height;
+    for (int v = 0; v < num_views; v++) {
+        const scoup_camera& c = cameras[v];
+        if (c.width != Wd || c.height != Hd) return fail(SCOUP_EINVAL, "cameras of one call must share width/height");
+        if (c.width <= 0 || c.height <= 0) return fail(SCOUP_EINVAL, "camera width/height <= 0");
+        if (!(c.fx > 0.f) || !(c.fy > 0.f) || !std::isfinite(c.fx) || !std::isfinite(c.fy) || !std::isfinite(c.cx) ||
+            !std::isfinite(c.cy))
+            return fail(SCOUP_EINVAL, "camera " + std::to_string(v) + ": bad intrinsics");
+        if (!rigid_ok(c.world_to_camera))
+            return fail(SCOUP_EDATA, "camera " + std::to_string(v) + ": world_to_camera is not rigid (1e-5)");
+    }
+    if ((int64_t)Wd * Hd >= (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "image too large");
+    if ((int64_t)((Wd + TILE - 1) / TILE + 1) * ((Hd + TILE - 1) / TILE + 1) > MAX_SAT_ENTRIES)
+        return fail(SCOUP_EUNSUPPORTED, "image too large for the tile tables (> 12288 16x16 tiles)");
+    const int64_t npx = (int64_t)Wd * Hd;
+    DeviceGuard dg(h->device);
+    if (h->G == 0) {
+        try {
+            CK(cudaMemsetAsync(out, 0, sizeof(float) * npx * h->L * num_views, h->stream));
+        } catch (const CudaError& e) {
+            return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+        }
+        return SCOUP_OK;
+    }
+    const Binning bn = choose_binning(Wd, Hd, h->bin_shift);
+    CallArgs args{nullptr, bn, nullptr, nullptr, num_views, 1, nullptr, npx, false};
+    args.render = true;
+    args.r_atoms = code_atoms;
+    args.r_coefs = code_coefs;
+    args.rK = K;
+    args.r_out = out;
+    return run_views(h, num_views, cameras, bn, npx, args, nullptr, 0);
+}
+
+scoup_status scoup_uplift_decode(scoup_uplift* h, int64_t num_pixels, const float* W_hat, const float* C, int32_t D,
+                                 float* F) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (num_pixels < 0 || D < 1) return fail(SCOUP_EINVAL, "bad sizes");
+    if (num_pixels == 0) return SCOUP_OK;
+    if (!W_hat || !C || !F) return fail(SCOUP_EINVAL, "NULL argument");
+    if (num_pixels > (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "num_pixels >= 2^31");
+    DeviceGuard dg(h->device);
+    if (!h->blas) {
+        if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) return fail(SCOUP_ECUDA, "cublasCreate failed");
+    }
+    cublasSetStream(h->blas, h->stream);
+    cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);  // fp32 throughout (no TF32)
+    // row-major F [P, D] = W_hat [P, L] C [L, D]  <=>  column-major F^T = C^T W_hat^T
+    const float one = 1.f, zero = 0.f;
+    const cublasStatus_t st = cublasSgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)num_pixels, h->L, &one, C, D,
+                                          W_hat, h->L, &zero, F, D);
+    if (st != CUBLAS_STATUS_SUCCESS) return fail(SCOUP_ECUDA, "cublasSgemm failed");
     return SCOUP_OK;
 }
 
@@ -1072,6 +1172,7 @@ void scoup_uplift_free(scoup_uplift* h) {
         dfree(h->W, h->stream);
         dfree(h->Z, h->stream);
     }
+    if (h->blas) cublasDestroy(h->blas);
     cudaStreamSynchronize(h->stream);
     delete h;
 }

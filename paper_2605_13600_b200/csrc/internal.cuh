@@ -264,6 +264,40 @@ __device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, fl
     return band_extent(a, e2, e3, Y0, Y1, xl, xr) && xr >= X0 && xl <= X1;
 }
 
+// DESIGN.md §3 exp2_spec for ycut <= y <= 0 (the caller's conservative prune guarantees
+// y >= ycut > -64, so the oracle's y < -64 branch is unreachable here).
+__device__ __forceinline__ float exp2_spec(float y) {
+    const float magic = 0x1.8p23f;
+    float t = __fadd_rn(y, magic);  // round-half-even to an integer
+    float kf = __fsub_rn(t, magic);
+    float f = __fsub_rn(y, kf);
+    float p = 0x1.5bba14p-10f;
+    p = __fmaf_rn(p, f, 0x1.3cea88p-7f);
+    p = __fmaf_rn(p, f, 0x1.c6b752p-5f);
+    p = __fmaf_rn(p, f, 0x1.ebf9bcp-3f);
+    p = __fmaf_rn(p, f, 0x1.62e42ap-1f);
+    p = __fmaf_rn(p, f, 1.0f);
+    // ldexp(p, k): bits(t) << 23 == k << 23 (mod 2^32) for t = 1.5*2^23 + k
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// One pixel of DESIGN.md §3 step PX for the record (a = mx, my, r, o; b = qa, qb, qc, ycut):
+// returns e (0 when the fragment does not contribute) and updates T (0 = finished pixel).
+// `live` gates the record (warp mask bit).  Shared by the uplift and render kernels.
+__device__ __forceinline__ float pixel_fragment(const float4& a, const float4& b, float px, float py, bool live,
+                                                float& T, bool& con) {
+    const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
+    const bool sq = live && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+    const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)), __fmul_rn(__fmul_rn(b.z, dy), dy));
+    const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
+    const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
+    const bool pass = sq && !(q > 0.f) && q >= b.w && al >= K_AMIN;
+    con = pass && !(Tn < K_TMIN);
+    const float e = con ? __fmul_rn(al, T) : 0.f;
+    T = con ? Tn : (pass ? 0.f : T);
+    return e;
+}
+
 // ---- launchers (kernels.cu) ----
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);
@@ -306,6 +340,12 @@ struct RasterParams {
     int chunk;                    // 0: first chunk (T starts at 1), else continue from Tstate
     bool count_tests;             // instrumented variant: count contributions and support tests
     bool dense;                   // dense features (Eq. 3 baseline): S == L, atom = slot, no atoms table
+    // render mode (Eq. 7, launch_render): per-pixel sum of the stored K-sparse codes
+    const uint32_t* r_atoms;      // [G, rK]
+    const float* r_coefs;
+    int rK;
+    float* r_out;                 // [views, H, W, L]: the batch's views start at r_view0
+    int64_t r_view0;
     int nlev;                            // semantic levels fused in this pass (1..MAX_LEV)
     const uint32_t* region_ids[MAX_VB][MAX_LEV];  // [H*W] per view and level
     int64_t code_row0[MAX_VB][MAX_LEV];  // first row of (view, level) in the combined code table
@@ -324,6 +364,7 @@ struct RasterParams {
     ErrorLatch err;
 };
 void launch_raster(const RasterParams& p, cudaStream_t s);
+void launch_render(const RasterParams& p, cudaStream_t s);
 
 void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
                  float* coefs, cudaStream_t s);

@@ -42,23 +42,6 @@ constexpr int NWARP = TILE_PIX / 32;
 #define RGROUP 4                              // records per warp-uniform branch in the pixel loop
 #endif
 
-// DESIGN.md §3 exp2_spec for ycut <= y <= 0 (the caller's conservative prune guarantees
-// y >= ycut > -64, so the oracle's y < -64 branch is unreachable here).
-__device__ __forceinline__ float exp2_spec(float y) {
-    const float magic = 0x1.8p23f;
-    float t = __fadd_rn(y, magic);  // round-half-even to an integer
-    float kf = __fsub_rn(t, magic);
-    float f = __fsub_rn(y, kf);
-    float p = 0x1.5bba14p-10f;
-    p = __fmaf_rn(p, f, 0x1.3cea88p-7f);
-    p = __fmaf_rn(p, f, 0x1.c6b752p-5f);
-    p = __fmaf_rn(p, f, 0x1.ebf9bcp-3f);
-    p = __fmaf_rn(p, f, 0x1.62e42ap-1f);
-    p = __fmaf_rn(p, f, 1.0f);
-    // ldexp(p, k): bits(t) << 23 == k << 23 (mod 2^32) for t = 1.5*2^23 + k
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
 // Sum e[i] over the lanes in the group (all lanes if !MASKED); lane l returns the sum for i = l.
 template <bool MASKED>
 __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool mine, int lane) {

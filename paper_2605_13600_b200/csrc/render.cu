@@ -1,0 +1,188 @@
+// render.cu -- sparse coefficient rendering (Eq. 7).
+//
+//   W_hat_v(p) = sum_{i in N_{v,p}} w_hat_i e_i(v,p)
+//
+// with the K-sparse stored codes w_hat_i (Eq. 6) and the same fragment weights e_i(v,p) as the
+// uplift -- the same depth chunks, candidate lists and DESIGN.md §3 per-pixel sequence
+// (pixel_fragment), so every e is bit-identical to the CPU oracle's.  One CTA of 256 threads per
+// (view, 16x16 tile), one pixel per thread; each pixel accumulates its dense L-vector in a padded
+// shared-memory row (a record's K (atom, coef) pairs are staged in shared memory per batch).  The
+// rows are carried between depth chunks through the output buffer itself: chunk 0 writes them
+// (zeros for tiles nothing reaches), later chunks add to them.
+#include "internal.cuh"
+
+namespace scoup {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int QCAP = 512;  // candidate ring (power of two >= 256 + BATCH)
+constexpr int NWARP = TILE_PIX / 32;
+constexpr int MAX_RK = 32;  // stored code length K
+
+struct RRing {
+    float4 q0[QCAP + BATCH];  // (mx, my, r, o)
+    float4 q1[QCAP + BATCH];  // (qa, qb, qc, ycut)
+    float4 q2[QCAP + BATCH];  // (support-box half-extents x, y, Gaussian id, sy)
+    float4 q3[QCAP + BATCH];  // band_relevant parameters
+};
+
+struct __align__(16) RSmem {
+    RRing r;
+    uint32_t code_a[BATCH][MAX_RK];  // the batch records' stored codes
+    float code_c[BATCH][MAX_RK];
+    int wcnt[NWARP];
+    // followed by the per-pixel accumulators: float acc[TILE_PIX][L + 1] (dynamic)
+};
+
+__global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RSmem& sm = *reinterpret_cast<RSmem*>(smem_raw);
+    float* const acc_base = reinterpret_cast<float*>(smem_raw + sizeof(RSmem));
+    const int L = p.L, LP = L + 1, rK = p.rK;
+    const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
+    const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
+    const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
+    const int64_t gtile = (int64_t)view * ntiles + tile;
+    if (p.chunk > 0 && !p.tile_live[gtile]) return;
+    const int bin = ((ty * TILE) >> p.bn.bshy) * p.bn.bins_x + ((tx * TILE) >> p.bn.bshx);
+    const uint2 range = p.ranges[view * p.bn.nbins() + bin];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int wx0 = tx * TILE + 8 * (warp & 1), wy0 = ty * TILE + 4 * (warp >> 1);
+    const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
+    const int Wd = p.width, Hd = p.height;
+    const bool inside = x < Wd && y < Hd;
+    float* Tpix = p.Tstate + (int64_t)view * Wd * Hd + (int64_t)y * Wd + x;
+    float* out_tile = p.r_out + ((p.r_view0 + view) * (int64_t)Hd * Wd) * L;  // this view's [H, W, L]
+    float* acc = acc_base + (int64_t)t * LP;                                  // my pixel's row
+
+    // the tile's rows: zero (chunk 0) or the partial sums of the earlier chunks
+    for (int i = t; i < TILE_PIX * L; i += TILE_PIX) {
+        const int pix = i / L, l = i - pix * L;
+        const int px_ = tx * TILE + 8 * ((pix >> 5) & 1) + (pix & 7);
+        const int py_ = ty * TILE + 4 * (pix >> 6) + ((pix >> 3) & 3);
+        float v = 0.f;
+        if (p.chunk > 0 && px_ < Wd && py_ < Hd) v = out_tile[((int64_t)py_ * Wd + px_) * L + l];
+        acc_base[pix * LP + l] = v;
+    }
+    const bool empty = range.x >= range.y;
+    float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
+
+    const float TX0 = (float)(tx * TILE) + 0.5f, TY0 = (float)(ty * TILE) + 0.5f;
+    const float TX1 = (float)(min(tx * TILE + TILE, Wd) - 1) + 0.5f;
+    const float TY1 = (float)(min(ty * TILE + TILE, Hd) - 1) + 0.5f;
+    const float WX0 = (float)wx0 + 0.5f, WY0 = (float)wy0 + 0.5f;
+    const float WX1 = (float)(min(wx0 + 8, Wd) - 1) + 0.5f, WY1 = (float)(min(wy0 + 4, Hd) - 1) + 0.5f;
+    const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    float4* const q0 = sm.r.q0;
+    float4* const q1 = sm.r.q1;
+    float4* const q2 = sm.r.q2;
+    float4* const q3 = sm.r.q3;
+    __syncthreads();
+
+    uint32_t cursor = range.x, q_head = 0, q_count = 0;
+    while (!empty) {
+        // ---- refill (as the uplift kernel: tile test, stable compaction into the ring)
+        while (q_count < (uint32_t)BATCH && cursor < range.y) {
+            const uint32_t idx = cursor + t;
+            bool accp = false;
+            float4 r0 = make_float4(0.f, 0.f, -1.f, 0.f), r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 r2 = make_float4(-1.f, -1.f, 0.f, 0.f), r3 = make_float4(0.f, 0.f, 0.f, -1.f);
+            if (idx < range.y) {
+                const uint32_t e = __ldg(p.eval + idx);
+                r0 = __ldg(p.rec0 + e);
+                r2 = __ldg(p.rec2 + e);
+                r3 = __ldg(p.rec3 + e);
+                accp = band_relevant(r0, r2, r3, TX0, TX1, TY0, TY1);
+                if (accp) r1 = __ldg(p.rec1 + e);
+            }
+            const unsigned bal = __ballot_sync(FULL, accp);
+            if (lane == 0) sm.wcnt[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t off = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < NWARP; w++) {
+                const uint32_t c = (uint32_t)sm.wcnt[w];
+                off += (w < warp) ? c : 0u;
+                tot += c;
+            }
+            if (accp) {
+                const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
+                q0[pos] = r0; q1[pos] = r1; q2[pos] = r2; q3[pos] = r3;
+                if (pos < (uint32_t)BATCH) {
+                    q0[pos + QCAP] = r0; q1[pos + QCAP] = r1; q2[pos + QCAP] = r2; q3[pos + QCAP] = r3;
+                }
+            }
+            q_count += tot;
+            cursor += TILE_PIX;
+            __syncthreads();
+        }
+        if (q_count == 0) break;
+        const uint32_t n = min((uint32_t)BATCH, q_count);
+        // ---- stage the batch records' stored codes (Eq. 6 output) in shared memory
+        for (int i = t; i < BATCH * rK; i += TILE_PIX) {
+            const int j = i / rK, k = i - j * rK;
+            uint32_t a = NONE;
+            float c = 0.f;
+            if ((uint32_t)j < n) {
+                const uint32_t g = __float_as_uint(q2[q_head + j].z);
+                a = __ldg(p.r_atoms + (int64_t)g * rK + k);
+                c = __ldg(p.r_coefs + (int64_t)g * rK + k);
+            }
+            sm.code_a[j][k] = a;
+            sm.code_c[j][k] = c;
+        }
+        __syncthreads();
+        // ---- per-warp mask, then the records in depth order; each contribution adds
+        //      coef * e to the pixel's row at its atoms (Eq. 7)
+        const bool warp_done = __all_sync(FULL, T == 0.f);
+        bool rel = false;
+        if (!warp_done && (uint32_t)lane < n)
+            rel = band_relevant(q0[q_head + lane], q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
+        const unsigned mask = __ballot_sync(FULL, rel);
+        for (int j = 0; j < BATCH; j++) {
+            if (!((mask >> j) & 1u)) continue;  // warp-uniform
+            bool con;
+            const float e = pixel_fragment(q0[q_head + j], q1[q_head + j], px, py, true, T, con);
+            if (con) {
+                for (int k = 0; k < rK; k++) {
+                    const uint32_t a = sm.code_a[j][k];
+                    if (a != NONE) acc[a] = __fadd_rn(acc[a], __fmul_rn(sm.code_c[j][k], e));
+                }
+            }
+        }
+        q_head = (q_head + n) & (QCAP - 1);
+        q_count -= n;
+        if (__syncthreads_count(T > 0.f) == 0) break;
+    }
+    __syncthreads();
+    // ---- rows out (coalesced along the L axis), state for the next chunk
+    for (int i = t; i < TILE_PIX * L; i += TILE_PIX) {
+        const int pix = i / L, l = i - pix * L;
+        const int px_ = tx * TILE + 8 * ((pix >> 5) & 1) + (pix & 7);
+        const int py_ = ty * TILE + 4 * (pix >> 6) + ((pix >> 3) & 3);
+        if (px_ < Wd && py_ < Hd) out_tile[((int64_t)py_ * Wd + px_) * L + l] = acc_base[pix * LP + l];
+    }
+    if (inside) *Tpix = T;
+    const int live = __syncthreads_count(T > 0.f);
+    if (t == 0) p.tile_live[gtile] = live > 0 ? 1 : 0;
+}
+
+}  // namespace
+
+size_t render_smem_bytes(int L) { return sizeof(RSmem) + (size_t)TILE_PIX * (L + 1) * sizeof(float); }
+
+void launch_render(const RasterParams& p, cudaStream_t s) {
+    const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
+    if (ntiles <= 0) return;
+    const size_t smem = render_smem_bytes(p.L);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    render_kernel<<<ntiles, TILE_PIX, smem, s>>>(p);
+}
+
+}  // namespace scoup

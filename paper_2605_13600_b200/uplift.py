@@ -89,6 +89,26 @@ class SparseUplift:
                                              out_coefs)
         return out_atoms, out_coefs
 
+    def render(self, cameras: Sequence, atoms, coefs, out=None):
+        """Eq. 7: per-pixel sum of the stored K-sparse codes w_hat_i e_i(v,p) -> [V, H, W, L] float32."""
+        torch = _torch()
+        cams = list(cameras)
+        if out is None:
+            out = torch.empty((len(cams), cams[0].height, cams[0].width, self.L), dtype=torch.float32,
+                              device=self.device)
+        abi.scoup_uplift_render_views(self._h, cams, atoms.contiguous(), coefs.contiguous(), int(atoms.shape[1]), out)
+        return out
+
+    def decode(self, W_hat, C, out=None):
+        """Eq. 8: F = W_hat C (codebook C [L, D]); W_hat [..., L] -> F [..., D] float32."""
+        torch = _torch()
+        P = W_hat.numel() // self.L
+        D = int(C.shape[1])
+        if out is None:
+            out = torch.empty(tuple(W_hat.shape[:-1]) + (D,), dtype=torch.float32, device=self.device)
+        abi.scoup_uplift_decode(self._h, P, W_hat.contiguous(), C.contiguous(), D, out)
+        return out
+
     def reset(self):
         abi.scoup_uplift_reset(self._h)
 
