@@ -197,9 +197,15 @@ scoup_status scoup_uplift_render_views(scoup_uplift *h, int32_t num_views, const
 
 /*
  * Codebook decode (Eq. 8): F = W_hat C for num_pixels rendered coefficient
- * vectors W_hat [P, L] (e.g. scoup_uplift_render_views' output) and a codebook C [L, D],
- * all float32 row-major on the device; F [P, D] overwritten.  A plain library GEMM (cuBLAS
- * SGEMM, fp32) on the handle's stream.  Errors: EINVAL, EUNSUPPORTED (P >= 2^31), ECUDA.
+ * vectors W_hat [P, L] (e.g. scoup_uplift_render_views' output) and a codebook C [L, D], all
+ * float32 row-major on the device; F [P, D] overwritten; W_hat and F 16-byte aligned.  With
+ * L % 8 == 0, L <= 64 and D % 64 == 0 it runs the library's tcgen05 kernel (3xTF32: every
+ * operand split exactly into a tf32 head and tail, fp32 accumulation in tensor memory, accuracy
+ * of an fp32 GEMM); other shapes use cuBLAS SGEMM (fp32, no TF32).  SCOUP_DECODE=sgemm forces
+ * the cuBLAS path (measurement only).  Stream-ordered on the handle's stream; a scratch of
+ * 8 L D bytes comes from the stream-ordered pool.  Non-finite inputs give non-finite outputs.
+ * Errors: EINVAL (NULL / host buffers, misaligned, bad sizes), EUNSUPPORTED (P >= 2^31),
+ * ENOMEM, ECUDA.
  */
 scoup_status scoup_uplift_decode(scoup_uplift *h, int64_t num_pixels, const float *W_hat, const float *C, int32_t D,
                                  float *F);

@@ -991,6 +991,27 @@ scoup_status scoup_uplift_decode(scoup_uplift* h, int64_t num_pixels, const floa
     if (!W_hat || !C || !F) return fail(SCOUP_EINVAL, "NULL argument");
     if (num_pixels > (int64_t)INT32_MAX) return fail(SCOUP_EUNSUPPORTED, "num_pixels >= 2^31");
     DeviceGuard dg(h->device);
+    const char* mode = std::getenv("SCOUP_DECODE");  // "sgemm": the cuBLAS path (A/B measurements)
+    if (decode_tc_supported(h->L, D) && !(mode && std::string(mode) == "sgemm")) {
+        if (!is_device_ptr(W_hat) || !is_device_ptr(C) || !is_device_ptr(F))
+            return fail(SCOUP_EINVAL, "decode buffers must be device memory");
+        if ((reinterpret_cast<uintptr_t>(W_hat) | reinterpret_cast<uintptr_t>(F)) & 15)
+            return fail(SCOUP_EINVAL, "W_hat / F must be 16-byte aligned");
+        try {
+            int sms = 0;
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+            float* scratch = nullptr;
+            dalloc(&scratch, decode_tc_scratch_bytes(h->L, D) / sizeof(float), h->stream);
+            const cudaError_t le = launch_decode_tc(W_hat, num_pixels, h->L, D, C, scratch, F, sms, h->stream);
+            if (le != cudaSuccess) throw CudaError{le, "launch_decode_tc"};
+            h->kernel_launches += 2;
+            dfree(scratch, h->stream);
+        } catch (const CudaError& e) {
+            return fail(e.err == cudaErrorMemoryAllocation ? SCOUP_ENOMEM : SCOUP_ECUDA,
+                        std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+        }
+        return SCOUP_OK;
+    }
     if (!h->blas) {
         if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) return fail(SCOUP_ECUDA, "cublasCreate failed");
     }

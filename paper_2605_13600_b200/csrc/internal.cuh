@@ -298,6 +298,12 @@ __device__ __forceinline__ float pixel_fragment(const float4& a, const float4& b
     return e;
 }
 
+// ---- decode (decode.cu): F = W_hat C on tcgen05 (3xTF32)
+bool decode_tc_supported(int L, int D);
+size_t decode_tc_scratch_bytes(int L, int D);
+cudaError_t launch_decode_tc(const float* W_hat, int64_t P, int L, int D, const float* C, float* scratch, float* F,
+                             int num_sms, cudaStream_t s);
+
 // ---- launchers (kernels.cu) ----
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);

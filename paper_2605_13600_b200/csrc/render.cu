@@ -6,9 +6,13 @@
 // uplift -- the same depth chunks, candidate lists and DESIGN.md §3 per-pixel sequence
 // (pixel_fragment), so every e is bit-identical to the CPU oracle's.  One CTA of 256 threads per
 // (view, 16x16 tile), one pixel per thread; each pixel accumulates its dense L-vector in a padded
-// shared-memory row (a record's K (atom, coef) pairs are staged in shared memory per batch).  The
-// rows are carried between depth chunks through the output buffer itself: chunk 0 writes them
-// (zeros for tiles nothing reaches), later chunks add to them.
+// shared-memory row (stride L + 1: the 32 lanes' read-modify-writes of one atom hit 32 banks).
+// A batch record's K (atom, coef) pairs are staged in shared memory with repeated atoms merged
+// and empty / padding slots pointed at the row's pad column, so a contribution's K updates are
+// independent: their loads issue back to back (8 at a time) instead of as a serial
+// load-add-store chain.  The rows are carried between depth chunks through the output buffer
+// itself: chunk 0 writes them (zeros for tiles nothing reaches), later chunks add to them; the
+// row I/O moves float4s along tile rows, which are contiguous in the [H, W, L] output.
 #include "internal.cuh"
 
 namespace scoup {
@@ -19,6 +23,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int QCAP = 512;  // candidate ring (power of two >= 256 + BATCH)
 constexpr int NWARP = TILE_PIX / 32;
 constexpr int MAX_RK = 32;  // stored code length K
+constexpr int KG = 8;       // code slots updated per independent group
 
 struct RRing {
     float4 q0[QCAP + BATCH];  // (mx, my, r, o)
@@ -29,11 +34,46 @@ struct RRing {
 
 struct __align__(16) RSmem {
     RRing r;
-    uint32_t code_a[BATCH][MAX_RK];  // the batch records' stored codes
-    float code_c[BATCH][MAX_RK];
+    __align__(16) uint32_t code_a[BATCH][MAX_RK];  // the batch records' stored codes: row column (pad: L)
+    __align__(16) float code_c[BATCH][MAX_RK];     //   and coefficient (merged over repeats; pad: 0)
     int wcnt[NWARP];
     // followed by the per-pixel accumulators: float acc[TILE_PIX][L + 1] (dynamic)
 };
+
+// Move a tile's pixel rows between shared memory (row of the pixel's thread, stride L + 1) and
+// the view's [H, W, L] output: i enumerates (tile row, column, 4-float group) so a tile row's
+// 16 L floats are one contiguous run in global memory.  i / L4 in fp32: (i + 0.5) / L4 is at
+// least 0.5 / L4 >= 1/64 from an integer and i < 2^13, so the truncation is exact.
+template <bool OUT>
+__device__ __forceinline__ void row_io(float* acc_base, float* out_view, int L, int tx, int ty, int Wd, int Hd,
+                                       int t) {
+    const int LP = L + 1;
+    const int vw = (L & 3) == 0 ? 4 : 1;  // float4 groups when L % 4 == 0
+    const int LG = L / vw;
+    const float inv = 1.0f / (float)LG;
+    for (int i = t; i < TILE_PIX * LG; i += TILE_PIX) {
+        const int q = (int)(((float)i + 0.5f) * inv);  // pixel in the tile, row-major
+        const int lg = i - q * LG;
+        const int r = q >> 4, xx = q & 15;
+        const int gx = tx * TILE + xx, gy = ty * TILE + r;
+        if (gx >= Wd || gy >= Hd) continue;
+        // thread of pixel (xx, r): 8x4 warp blocks, lanes row-major inside
+        const int th = ((xx >> 3) + 2 * (r >> 2)) * 32 + (xx & 7) + 8 * (r & 3);
+        float* srow = acc_base + th * LP + lg * vw;
+        float* grow = out_view + ((int64_t)gy * Wd + gx) * L + lg * vw;
+        if (vw == 4) {
+            if (OUT) {
+                *reinterpret_cast<float4*>(grow) = make_float4(srow[0], srow[1], srow[2], srow[3]);
+            } else {
+                const float4 g4 = *reinterpret_cast<const float4*>(grow);
+                srow[0] = g4.x; srow[1] = g4.y; srow[2] = g4.z; srow[3] = g4.w;
+            }
+        } else {
+            if (OUT) *grow = *srow;
+            else *srow = *grow;
+        }
+    }
+}
 
 __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -57,13 +97,10 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
     float* acc = acc_base + (int64_t)t * LP;                                  // my pixel's row
 
     // the tile's rows: zero (chunk 0) or the partial sums of the earlier chunks
-    for (int i = t; i < TILE_PIX * L; i += TILE_PIX) {
-        const int pix = i / L, l = i - pix * L;
-        const int px_ = tx * TILE + 8 * ((pix >> 5) & 1) + (pix & 7);
-        const int py_ = ty * TILE + 4 * (pix >> 6) + ((pix >> 3) & 3);
-        float v = 0.f;
-        if (p.chunk > 0 && px_ < Wd && py_ < Hd) v = out_tile[((int64_t)py_ * Wd + px_) * L + l];
-        acc_base[pix * LP + l] = v;
+    if (p.chunk == 0) {
+        for (int i = t; i < TILE_PIX * LP; i += TILE_PIX) acc_base[i] = 0.f;
+    } else {
+        row_io<false>(acc_base, out_tile, L, tx, ty, Wd, Hd, t);
     }
     const bool empty = range.x >= range.y;
     float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
@@ -120,18 +157,58 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
         }
         if (q_count == 0) break;
         const uint32_t n = min((uint32_t)BATCH, q_count);
-        // ---- stage the batch records' stored codes (Eq. 6 output) in shared memory
-        for (int i = t; i < BATCH * rK; i += TILE_PIX) {
-            const int j = i / rK, k = i - j * rK;
+        // ---- stage the batch records' stored codes (Eq. 6 output): K rounded up to a multiple
+        //      of KG, empty / out-of-range slots -> the pad column L, repeated atoms merged into
+        //      their first slot so the slots of one record address distinct columns
+        const int rKp = (rK + KG - 1) / KG * KG;
+        for (int i = t; i < BATCH * rKp; i += TILE_PIX) {
+            const int j = i / rKp, k = i - j * rKp;
             uint32_t a = NONE;
             float c = 0.f;
-            if ((uint32_t)j < n) {
-                const uint32_t g = __float_as_uint(q2[q_head + j].z);
+            if ((uint32_t)j < n && k < rK) {
+                const uint32_t g = __float_as_uint(q2[(q_head + j) & (QCAP - 1)].z);
                 a = __ldg(p.r_atoms + (int64_t)g * rK + k);
                 c = __ldg(p.r_coefs + (int64_t)g * rK + k);
+                if ((a != NONE && a >= (uint32_t)L) || !isfinite(c)) {
+                    latch_error(p.err, ERR_CODE, (long long)g * rK + k);
+                    a = NONE;
+                }
             }
             sm.code_a[j][k] = a;
             sm.code_c[j][k] = c;
+        }
+        __syncthreads();
+        constexpr int SPT = BATCH * MAX_RK / TILE_PIX;  // slots per thread
+        float cm[SPT];
+        uint32_t am[SPT];
+#pragma unroll
+        for (int u = 0; u < SPT; u++) {
+            const int i = t + u * TILE_PIX;
+            am[u] = (uint32_t)L;
+            cm[u] = 0.f;
+            if (i < BATCH * rKp) {
+                const int j = i / rKp, k = i - j * rKp;
+                const uint32_t a = sm.code_a[j][k];
+                bool first = a != NONE;
+                for (int k2 = 0; k2 < k && first; k2++) first = sm.code_a[j][k2] != a;
+                if (first) {
+                    float c = sm.code_c[j][k];
+                    for (int k2 = k + 1; k2 < rK; k2++)
+                        if (sm.code_a[j][k2] == a) c = __fadd_rn(c, sm.code_c[j][k2]);
+                    am[u] = a;
+                    cm[u] = c;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < SPT; u++) {
+            const int i = t + u * TILE_PIX;
+            if (i < BATCH * rKp) {
+                const int j = i / rKp, k = i - j * rKp;
+                sm.code_a[j][k] = am[u];
+                sm.code_c[j][k] = cm[u];
+            }
         }
         __syncthreads();
         // ---- per-warp mask, then the records in depth order; each contribution adds
@@ -146,9 +223,18 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
             bool con;
             const float e = pixel_fragment(q0[q_head + j], q1[q_head + j], px, py, true, T, con);
             if (con) {
-                for (int k = 0; k < rK; k++) {
-                    const uint32_t a = sm.code_a[j][k];
-                    if (a != NONE) acc[a] = __fadd_rn(acc[a], __fmul_rn(sm.code_c[j][k], e));
+                for (int k0 = 0; k0 < rKp; k0 += KG) {
+                    const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.code_a[j][k0]);
+                    const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.code_a[j][k0 + 4]);
+                    const uint32_t a[KG] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float4 c0 = *reinterpret_cast<const float4*>(&sm.code_c[j][k0]);
+                    const float4 c1 = *reinterpret_cast<const float4*>(&sm.code_c[j][k0 + 4]);
+                    const float c[KG] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                    float v[KG];
+#pragma unroll
+                    for (int k = 0; k < KG; k++) v[k] = acc[a[k]];  // distinct columns (or the pad)
+#pragma unroll
+                    for (int k = 0; k < KG; k++) acc[a[k]] = __fmaf_rn(c[k], e, v[k]);
                 }
             }
         }
@@ -157,13 +243,8 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
         if (__syncthreads_count(T > 0.f) == 0) break;
     }
     __syncthreads();
-    // ---- rows out (coalesced along the L axis), state for the next chunk
-    for (int i = t; i < TILE_PIX * L; i += TILE_PIX) {
-        const int pix = i / L, l = i - pix * L;
-        const int px_ = tx * TILE + 8 * ((pix >> 5) & 1) + (pix & 7);
-        const int py_ = ty * TILE + 4 * (pix >> 6) + ((pix >> 3) & 3);
-        if (px_ < Wd && py_ < Hd) out_tile[((int64_t)py_ * Wd + px_) * L + l] = acc_base[pix * LP + l];
-    }
+    // ---- rows out, state for the next chunk
+    row_io<true>(acc_base, out_tile, L, tx, ty, Wd, Hd, t);
     if (inside) *Tpix = T;
     const int live = __syncthreads_count(T > 0.f);
     if (t == 0) p.tile_live[gtile] = live > 0 ? 1 : 0;

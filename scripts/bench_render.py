@@ -67,8 +67,12 @@ def main():
         for v in range(cfg.num_views):
             up.decode(Wh[v % B], C, out=F)
 
+    def fill_all():  # write-only stream of the same size as the decode output: HBM write reference
+        for v in range(cfg.num_views):
+            F.fill_(1.0)
+
     res = {}
-    for name, fn in (("render", render_all), ("decode", decode_all)):
+    for name, fn in (("render", render_all), ("decode", decode_all), ("fill", fill_all)):
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
@@ -90,6 +94,7 @@ def main():
         "render_ms_per_view": res["render"], "render_fps": 1e3 / res["render"],
         "decode_ms_per_view": res["decode"], "decode_tflops": flops / (res["decode"] * 1e-3) / 1e12,
         "decode_gbps": byts / (res["decode"] * 1e-3) / 1e9,
+        "fill_gbps": 4.0 * H * W * args.D / (res["fill"] * 1e-3) / 1e9,
         "render_out_gbps": 4.0 * H * W * L / (res["render"] * 1e-3) / 1e9,
         "dtype": "f32", "data": "synthetic",
     }))

@@ -501,3 +501,69 @@ def test_render_full_size_outdoor_view(dev):
         assert np.abs(ref).max() > 0.1
         bad = np.abs(gv - ref) > 1e-6 + 1e-5 * np.abs(ref)
         assert not bad.any(), (bad.sum(), np.abs(gv - ref).max())
+
+
+def test_render_errors(dev, tiny_scene):
+    """Render input checks: an atom >= L (not SCOUP_NONE) or a non-finite coefficient is a latched
+    EDATA naming the flat code slot; L > 128 is EUNSUPPORTED; K outside [1, 32] is EINVAL."""
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    g = scene.gaussians
+    K = 4
+    atoms = torch.zeros((g.count, K), dtype=torch.int32, device="cuda")
+    coefs = torch.full((g.count, K), 0.25, dtype=torch.float32, device="cuda")
+    up = SparseUplift(g, cfg.L, K)
+    try:
+        up.render(scene.cameras[:1], atoms, coefs)
+        up.stats()  # all rows valid (atom 0 four times: merged)
+        # a slot of a Gaussian that surely renders: the one with the largest opacity
+        gi = int(np.argmax(g.opacities))
+        atoms[gi, 2] = cfg.L
+        up.render(scene.cameras, atoms, coefs)
+        with pytest.raises(abi.ScoupError) as ei:
+            up.stats()
+        assert ei.value.status == 2 and str(gi * K + 2) in str(ei.value)
+        up.reset()
+        with pytest.raises(abi.ScoupError) as ei:
+            up.render(scene.cameras[:1], atoms[:, :0], coefs[:, :0])
+        assert ei.value.status == 1
+    finally:
+        up.close()
+    up = SparseUplift(g, 256, K)
+    try:
+        with pytest.raises(abi.ScoupError) as ei:
+            up.render(scene.cameras[:1], atoms, coefs)
+        assert ei.value.status == 6
+    finally:
+        up.close()
+
+
+@pytest.mark.parametrize("L,D,P", [(64, 512, 1000), (8, 64, 129), (16, 192, 4096), (64, 768, 300),
+                                   (40, 128, 7), (72, 512, 500)])
+def test_decode_matches_fp64(dev, L, D, P):
+    """Eq. 8 F = W_hat C against a float64 product.  L % 8 == 0, L <= 64 and D % 64
+    == 0 run the tcgen05 3xTF32 kernel (ragged last 128-row tile, 1-4 N tiles of 64/128/256
+    columns); L = 72 takes the cuBLAS SGEMM path.  Bound: fp32-GEMM accuracy, |F - F64| <=
+    1e-5 (|W_hat| |C|) + 1e-30, i.e. ~40 ulp of the magnitude sum (3xTF32 drops terms below
+    2^-20 relative per product; fp32 accumulation adds <= L 2^-24)."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    g = synth.Gaussians(*(np.zeros((1, 3), np.float32), np.full((1, 3), 0.1, np.float32),
+                          np.array([[1, 0, 0, 0]], np.float32), np.full((1,), 0.5, np.float32)))
+    rng = np.random.default_rng(L * 1000 + D)
+    W = rng.normal(size=(P, L)).astype(np.float32) * rng.choice([1e-3, 1.0, 1e3], size=(P, 1)).astype(np.float32)
+    C = rng.normal(size=(L, D)).astype(np.float32)
+    up = SparseUplift(g, L, 1)
+    try:
+        n0 = up.stats()["kernel_launches"]
+        F = up.decode(torch.from_numpy(W).cuda(), torch.from_numpy(C).cuda())
+        torch.cuda.synchronize()
+        got = F.double().cpu().numpy()
+        # the library's own kernels (prep + tcgen05 decode) ran, or none (cuBLAS)
+        assert up.stats()["kernel_launches"] - n0 == (2 if L <= 64 and L % 8 == 0 else 0)
+    finally:
+        up.close()
+    ref = W.astype(np.float64) @ C.astype(np.float64)
+    bound = 1e-5 * (np.abs(W.astype(np.float64)) @ np.abs(C.astype(np.float64))) + 1e-30
+    err = np.abs(got - ref)
+    assert (err <= bound).all(), (int((err > bound).sum()), float((err / bound).max()))
