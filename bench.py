@@ -285,6 +285,7 @@ def main():
     tests_step = sum_over_ranks(st0["support_tests"])
     entries_step = sum_over_ranks(st0["tile_entries"])
     visible_step = sum_over_ranks(st0["visible"])
+    lane_evals_step = sum_over_ranks(st0["lane_evaluations"])
 
     up.set_timing(True)
     barrier()
@@ -370,6 +371,8 @@ def main():
                            sum(m.numel() for m in maps_l) * 4 / 1e9, nlev * Npad * L * 4 / 1e6)},
             "contributions_per_step": int(contrib_step),
             "support_tests_per_step": int(tests_step),
+            "lane_evaluations_per_step": int(lane_evals_step),
+            "raster_lane_use": tests_step / max(1, lane_evals_step),
             "bin_entries_per_step": int(entries_step),
             "visible_per_step": int(visible_step),
             "device_ms_per_step": {k: tm[k] / args.steps for k in ("preprocess_ms", "binning_ms", "raster_ms", "topk_ms")},

@@ -78,6 +78,9 @@ typedef struct {
                                only while scoup_uplift_set_counters(h, 1) is on */
     int64_t kernel_launches;/* launches of this library's own kernels (CUB sort/scan excluded) */
     int64_t cub_launches;   /* CUB device-wide sort/scan calls */
+    int64_t lane_evaluations; /* lanes that ran the per-pixel sequence on a record (32 per
+                                 (warp, record) evaluated; counted with the support tests):
+                                 support_tests / lane_evaluations is the raster's lane use */
 } scoup_stats;
 
 /* Per-kernel-class device time (CUDA events on the launching streams), accumulated while

@@ -35,7 +35,7 @@ class scoup_camera(C.Structure):
 class scoup_stats(C.Structure):
     _fields_ = [("views", C.c_int64), ("contributions", C.c_int64), ("tile_entries", C.c_int64),
                 ("visible", C.c_int64), ("support_tests", C.c_int64), ("kernel_launches", C.c_int64),
-                ("cub_launches", C.c_int64)]
+                ("cub_launches", C.c_int64), ("lane_evaluations", C.c_int64)]
 
 
 class scoup_timing(C.Structure):

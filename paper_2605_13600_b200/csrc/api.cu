@@ -144,7 +144,7 @@ struct scoup_uplift {
     PackedGaussians pg{};
     int* d_err_code = nullptr;
     long long* d_err_index = nullptr;
-    unsigned long long* d_stats = nullptr;  // views, contributions, entries, visible
+    unsigned long long* d_stats = nullptr;  // views, contributions, (unused), visible, support tests, lane evaluations
     Ctx ctx[2];
     uint32_t* code_atoms = nullptr;
     float* code_coefs = nullptr;
@@ -550,6 +550,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.Z = h->Z;
     p.contrib_ctr = h->d_stats + 1;
     p.support_ctr = h->d_stats + 4;
+    p.lane_eval_ctr = h->d_stats + 5;
     p.err = latch_of(h);
     ev_mark(c, mark0);
     if (a.render) launch_render(p, c.s);
@@ -751,10 +752,10 @@ scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num
         }
         dalloc(&h->d_err_code, 1, hs);
         dalloc(&h->d_err_index, 1, hs);
-        dalloc(&h->d_stats, 5, hs);
+        dalloc(&h->d_stats, 6, hs);
         CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
         CK(cudaMemsetAsync(h->d_err_index, 0, sizeof(long long), h->stream));
-        CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->d_stats, 0, 6 * sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->W, 0, sizeof(float) * rows_padded * L * num_levels, h->stream));
         CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * rows_padded, h->stream));
         const int64_t G = std::max<int64_t>(1, num_gaussians);
@@ -1091,7 +1092,7 @@ scoup_status scoup_uplift_reset(scoup_uplift* h) {
         DeviceGuard dg(h->device);
         CK(cudaMemsetAsync(h->W, 0, sizeof(float) * std::max<int64_t>(1, h->Npad) * h->L * h->nlev, h->stream));
         CK(cudaMemsetAsync(h->Z, 0, sizeof(float) * std::max<int64_t>(1, h->Npad), h->stream));
-        CK(cudaMemsetAsync(h->d_stats, 0, 5 * sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->d_stats, 0, 6 * sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->d_err_code, 0, sizeof(int), h->stream));
         h->latched = false;
         h->host_entries = 0;
@@ -1116,7 +1117,7 @@ scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
     if (!h || !out) return fail(SCOUP_EINVAL, "NULL argument");
     try {
         DeviceGuard dg(h->device);
-        unsigned long long s[5];
+        unsigned long long s[6];
         CK(cudaStreamSynchronize(h->stream));
         CK(cudaMemcpy(s, h->d_stats, sizeof(s), cudaMemcpyDeviceToHost));
         out->views = (int64_t)s[0];
@@ -1126,6 +1127,7 @@ scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
         out->support_tests = (int64_t)s[4];
         out->kernel_launches = h->kernel_launches;
         out->cub_launches = h->cub_launches;
+        out->lane_evaluations = (int64_t)s[5];
         return check_latched(h);
     } catch (const CudaError& e) {
         return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));

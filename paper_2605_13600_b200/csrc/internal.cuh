@@ -367,6 +367,7 @@ struct RasterParams {
     float* Z;
     unsigned long long* contrib_ctr;  // handle stats
     unsigned long long* support_ctr;  // handle stats: support tests
+    unsigned long long* lane_eval_ctr;  // handle stats: lane evaluations (32 per warp-record)
     ErrorLatch err;
 };
 void launch_raster(const RasterParams& p, cudaStream_t s);

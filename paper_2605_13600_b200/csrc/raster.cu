@@ -128,6 +128,7 @@ struct __align__(16) Smem {
     int overflow;
     unsigned long long contrib;
     unsigned long long tests;
+    unsigned long long evals;
 };
 
 
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             key[l] = rid;
         }
     }
-    if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; }
+    if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; sm.evals = 0ull; }
     if (t < MAX_SLOTS) sm.slot_key[t][0] = SLOT_EMPTY;
     for (int i = t; i < 3 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
     if (t < 3 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
     // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
     float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
-    uint32_t cnt = 0, tests = 0;
+    uint32_t cnt = 0, tests = 0, wevals = 0;
     const int L = p.L;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -365,7 +366,10 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
                 // (a finished pixel, T == 0, needs no test of its own: its Tn = 0 < 1e-4 makes
                 // every later fragment a non-contributing stop that leaves T = 0)
-                const bool sq = ((mask >> j) & 1u) && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                // (the record's warp-mask bit is only needed for the support-test count: a
+                // record outside the mask cannot pass the alpha test anywhere in the block --
+                // band_relevant is conservative -- so it is a no-op for every lane)
+                const bool sq = (!COUNT || ((mask >> j) & 1u)) && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
                 const bool active = COUNT && T > 0.f;
                 const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
                                           __fmul_rn(__fmul_rn(b.z, dy), dy));
@@ -385,6 +389,12 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const bool any = COUNT ? cbits != 0u : mask != 0u;
         cnt += __popc(cbits);
         tests += __popc(tbits);
+        if (COUNT) {  // records this warp evaluated (whole groups: the branch is per group)
+            unsigned gm = 0u;
+#pragma unroll
+            for (int g0 = 0; g0 < BATCH; g0 += RGROUP) gm += ((mask >> g0) & ((1u << RGROUP) - 1u)) ? RGROUP : 0u;
+            wevals += gm;
+        }
         if (overflow && any) {
             // per-pixel reductions straight from the code table (tiles with > MAX_SLOTS tuples)
 #pragma unroll
@@ -496,6 +506,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     if (COUNT) {
         const unsigned ts = __reduce_add_sync(FULL, tests);
         if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
+        if (lane == 0 && wevals) atomicAdd(&sm.evals, 32ull * wevals);
     }
     __syncthreads();
     if (t == 0) {
@@ -504,6 +515,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             if (p.contrib_out[view]) atomicAdd(reinterpret_cast<unsigned long long*>(p.contrib_out[view]), sm.contrib);
         }
         if (COUNT && sm.tests) atomicAdd(p.support_ctr, sm.tests);
+        if (COUNT && sm.evals) atomicAdd(p.lane_eval_ctr, sm.evals);
     }
 }
 
