@@ -347,3 +347,38 @@ class Scene:
 
 def make_scene(cfg: SceneConfig, seed: int = 0) -> Scene:
     return Scene(cfg, make_gaussians(cfg, seed), make_cameras(cfg, seed), seed)
+
+
+# ---- 2D sparse coding inputs (Eq. 4) ----------
+
+@dataclass
+class RegionFeatures:
+    """Per-region feature rows (CLIP stand-ins) and, for tests, the planted structure."""
+    F: np.ndarray          # [R, D] float32, unit rows
+    C_true: np.ndarray     # [L_true, D] float32 unit rows
+    atoms: np.ndarray      # [R, K] planted atoms
+    coefs: np.ndarray      # [R, K] planted convex weights
+
+
+def make_region_features(R: int, D: int, L_true: int, K: int, noise: float = 0.01,
+                         seed: int = 0) -> RegionFeatures:
+    """R region features that are K-sparse convex combinations of a random unit codebook plus
+    Gaussian noise (SPEC S:225's generator), normalised to unit length like CLIP embeddings."""
+    rng = _rng(seed, 77)
+    C = rng.normal(size=(L_true, D))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    atoms = np.stack([rng.choice(L_true, size=K, replace=False) for _ in range(R)])
+    coefs = rng.dirichlet(np.ones(K), size=R)
+    F = np.einsum("rk,rkd->rd", coefs, C[atoms]) + noise * rng.normal(size=(R, D))
+    F /= np.linalg.norm(F, axis=1, keepdims=True)
+    return RegionFeatures(F.astype(np.float32), C.astype(np.float32), atoms, coefs)
+
+
+def make_kmeans_draws(L: int, D: int, seed: int = 0):
+    """The random numbers k-means++ draws (R-SC6): L uniforms in [0, 1) and L unit fallback
+    vectors, generated here and passed to both implementations."""
+    rng = _rng(seed, 78)
+    u = rng.uniform(size=L)
+    E = rng.normal(size=(L, D))
+    E /= np.linalg.norm(E, axis=1, keepdims=True)
+    return u, E.astype(np.float32)
