@@ -48,7 +48,10 @@ EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_vi
            "scoup_uplift_render_views", "scoup_uplift_decode",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
-           "scoup_uplift_free", "scoup_last_error", "scoup_version"]
+           "scoup_uplift_free", "scoup_last_error", "scoup_version",
+           # include/scoup_sparse_coding.h
+           "scoup_sc_init", "scoup_sc_kmeans", "scoup_sc_set_state", "scoup_sc_get_state", "scoup_sc_train",
+           "scoup_sc_encode", "scoup_sc_free"]
 
 _lib = None
 
@@ -78,11 +81,18 @@ def lib():
         L.scoup_uplift_free.argtypes = [P]
         L.scoup_uplift_free.restype = None
         L.scoup_last_error.restype = C.c_char_p
+        L.scoup_sc_init.argtypes = [C.c_int, P, i64, i32, i32, i32, P, C.POINTER(P)]
+        L.scoup_sc_kmeans.argtypes = [P, P, P, i32, C.POINTER(i32)]
+        L.scoup_sc_set_state.argtypes = [P, P, P, P, P, P, P, i64]
+        L.scoup_sc_get_state.argtypes = [P] + [C.POINTER(P)] * 6 + [C.POINTER(i64)]
+        L.scoup_sc_train.argtypes = [P, i32, C.c_float, C.c_float, C.c_float, C.c_float, P]
+        L.scoup_sc_encode.argtypes = [P, P, P]
+        L.scoup_sc_free.argtypes = [P]
+        L.scoup_sc_free.restype = None
         L.scoup_version.restype = C.c_char_p
         for name in ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
                      "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
                      "scoup_uplift_render_views", "scoup_uplift_decode",
-           "scoup_uplift_render_views", "scoup_uplift_decode",
                      "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
                      "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
             getattr(L, name).restype = C.c_int
@@ -230,3 +240,44 @@ def scoup_last_error() -> str:
 
 def scoup_version() -> str:
     return lib().scoup_version().decode()
+
+
+# ---- 2D sparse coding (include/scoup_sparse_coding.h) -------------------------------------------
+
+def scoup_sc_init(device: int, stream: int, R: int, D: int, L: int, K: int, features) -> int:
+    h = C.c_void_p()
+    _check(lib().scoup_sc_init(device, stream or None, R, D, L, K, ptr(features), C.byref(h)))
+    return h.value
+
+
+def scoup_sc_kmeans(h: int, uniforms, fallback, max_iter: int) -> int:
+    import numpy as np
+    u = np.ascontiguousarray(uniforms, dtype=np.float64)
+    fb = fallback if hasattr(fallback, "data_ptr") else np.ascontiguousarray(fallback, dtype=np.float32)
+    it = C.c_int32(0)
+    _check(lib().scoup_sc_kmeans(h, u.ctypes.data, ptr(fb), max_iter, C.byref(it)))
+    return it.value
+
+
+def scoup_sc_set_state(h: int, C_=None, Z=None, mC=None, vC=None, mZ=None, vZ=None, t: int = 0) -> None:
+    _check(lib().scoup_sc_set_state(h, ptr(C_), ptr(Z), ptr(mC), ptr(vC), ptr(mZ), ptr(vZ), t))
+
+
+def scoup_sc_get_state(h: int):
+    ps = [C.c_void_p() for _ in range(6)]
+    t = C.c_int64(0)
+    _check(lib().scoup_sc_get_state(h, *[C.byref(x) for x in ps], C.byref(t)))
+    return [x.value for x in ps], t.value
+
+
+def scoup_sc_train(h: int, epochs: int, lr: float, beta1: float, beta2: float, eps: float, loss_out=None) -> None:
+    _check(lib().scoup_sc_train(h, epochs, lr, beta1, beta2, eps, ptr(loss_out)))
+
+
+def scoup_sc_encode(h: int, atoms, coefs) -> None:
+    _check(lib().scoup_sc_encode(h, ptr(atoms), ptr(coefs)))
+
+
+def scoup_sc_free(h: int) -> None:
+    if h:
+        lib().scoup_sc_free(h)

@@ -4,11 +4,13 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu", "decode.cu"]
+SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu", "decode.cu", "sparse_coding.cu"]
 HEADERS = ["internal.cuh"]
 LIB = os.path.join(HERE, "libscoup.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -19,7 +21,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     # parity-critical arithmetic uses explicit _rn intrinsics; also forbid contraction
     "-fmad=false",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
 ]
 
@@ -27,6 +29,7 @@ NVCC_FLAGS = [
 def _inputs():
     paths = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     paths.append(os.path.join(ROOT, "include", "scoup.h"))
+    paths.append(os.path.join(ROOT, "include", "scoup_sparse_coding.h"))
     paths.append(os.path.abspath(__file__))
     return paths
 
@@ -43,12 +46,22 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     if not force and out == LIB and not defines and not stale():
         return LIB
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lcublas"]
+    flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        flags.insert(0, "-Xptxas=-v")
+    with tempfile.TemporaryDirectory(prefix="scoup_build_") as td:
+        def compile_one(src: str) -> str:
+            obj = os.path.join(td, os.path.splitext(src)[0] + ".o")
+            cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.check_call(cmd)
+            return obj
+        # translation units compile in parallel, then one device-aware link
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            objs = list(ex.map(compile_one, SOURCES))
+        subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                               "-o", tmp, *objs, "-lcublas"])
     os.replace(tmp, out)
     return out
 

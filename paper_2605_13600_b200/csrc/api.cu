@@ -685,6 +685,8 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
 
 }  // namespace
 
+void scoup::set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
 extern "C" {
 
 const char* scoup_last_error(void) { return g_last_error.c_str(); }

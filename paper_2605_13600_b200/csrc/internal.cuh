@@ -298,6 +298,9 @@ __device__ __forceinline__ float pixel_fragment(const float4& a, const float4& b
     return e;
 }
 
+// thread-local message returned by scoup_last_error() (api.cu)
+void set_last_error(const char* msg);
+
 // ---- decode (decode.cu): F = W_hat C on tcgen05 (3xTF32)
 bool decode_tc_supported(int L, int D);
 size_t decode_tc_scratch_bytes(int L, int D);

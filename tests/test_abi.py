@@ -1,4 +1,4 @@
-"""The C-ABI library builds, loads and exports every symbol include/scoup.h declares.
+"""The C-ABI library builds, loads and exports every symbol include/*.h declares.
 Host-side argument validation is exercised without a GPU (no compute calls)."""
 import ctypes as C
 import os
@@ -10,7 +10,7 @@ import pytest
 from paper_2605_13600_b200 import abi, build
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "scoup.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("scoup.h", "scoup_sparse_coding.h")]
 
 
 @pytest.fixture(scope="module")
@@ -20,7 +20,7 @@ def lib():
 
 
 def declared_functions():
-    src = open(HEADER).read()
+    src = "\n".join(open(h).read() for h in HEADERS)
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(scoup_\w+)\s*\(", src)))
 
