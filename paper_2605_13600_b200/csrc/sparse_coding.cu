@@ -29,7 +29,10 @@ namespace scoup {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int SC_THREADS = 512;  // 16 warps, one region at a time each
+// threads of the epoch kernel: 32 warps (one region at a time each) hide the dependent loads
+// best; the wide instantiations (KMAX or DPL of 32) need more registers and run 16 warps
+template <int DPL, int KMAX>
+constexpr int sc_threads() { return (KMAX >= 32 || DPL >= 32) ? 512 : 1024; }
 constexpr int MAX_DPL = 32;      // D <= 1024
 constexpr int MAX_LPL = 4;       // L <= 128
 constexpr int SC_MAX_K = 32;
@@ -92,21 +95,21 @@ __device__ __forceinline__ void warp_topk(const float (&z)[LPL], int K, int lane
     }
 }
 
-template <int DPL, int LPL, int KMAX>
-__global__ void __launch_bounds__(SC_THREADS) sc_epoch_kernel(ScDev p) {
+template <int DPL, int LPL, int KMAX, int NT = sc_threads<DPL, KMAX>()>
+__global__ void __launch_bounds__(NT) sc_epoch_kernel(ScDev p) {
     extern __shared__ float sgC[];  // [L * D] this CTA's codebook gradient
-    __shared__ float sloss[SC_THREADS / 32];
+    __shared__ float sloss[NT / 32];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int D = p.D, L = p.L, K = p.K, LD = L * D;
-    for (int i = t; i < LD; i += SC_THREADS) sgC[i] = 0.f;
+    for (int i = t; i < LD; i += NT) sgC[i] = 0.f;
     __syncthreads();
     const long long step = *p.step + 1;
     const float bc1 = (float)(1.0 - pow((double)p.b1, (double)step));
     const float bc2 = (float)(1.0 - pow((double)p.b2, (double)step));
     const float invR = 1.0f / (float)p.R;
     float lossacc = 0.f;
-    const int64_t nw = (int64_t)gridDim.x * (SC_THREADS / 32);
-    for (int64_t r = (int64_t)blockIdx.x * (SC_THREADS / 32) + warp; r < p.R; r += nw) {
+    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t r = (int64_t)blockIdx.x * (NT / 32) + warp; r < p.R; r += nw) {
         float z[LPL];
 #pragma unroll
         for (int i = 0; i < LPL; i++) {
@@ -125,6 +128,11 @@ __global__ void __launch_bounds__(SC_THREADS) sc_epoch_kernel(ScDev p) {
         }
 #pragma unroll
         for (int k = 0; k < KMAX; k++) w[k] /= wsum;
+        // the kept codebook rows: re-read (L1/L2) for the backward pass, or kept in registers
+        // when the 512-thread instantiation leaves room (KMAX * DPL <= 64)
+        constexpr bool CACHE = NT <= 512 && KMAX * DPL <= 64;
+        float cv[CACHE ? KMAX : 1][CACHE ? DPL : 1];
+        const float* Cr = p.C;
         float f[DPL], x[DPL];
         float xf = 0.f, xx = 0.f, ff = 0.f;
 #pragma unroll
@@ -135,7 +143,11 @@ __global__ void __launch_bounds__(SC_THREADS) sc_epoch_kernel(ScDev p) {
             if (d < D) {
 #pragma unroll
                 for (int k = 0; k < KMAX; k++)
-                    if (k < K) acc = fmaf(w[k], p.C[(int64_t)sel[k] * D + d], acc);
+                    if (k < K) {
+                        const float c = __ldg(Cr + (int64_t)sel[k] * D + d);
+                        if (CACHE) cv[CACHE ? k : 0][CACHE ? i : 0] = c;
+                        acc = fmaf(w[k], c, acc);
+                    }
             }
             x[i] = acc;
             xf = fmaf(acc, f[i], xf);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(SC_THREADS) sc_epoch_kernel(ScDev p) {
             for (int k = 0; k < KMAX; k++) {
                 if (k >= K) continue;
                 const int ci = sel[k] * D + d;
-                gw[k] = fmaf(g, p.C[ci], gw[k]);
+                gw[k] = fmaf(g, CACHE ? cv[CACHE ? k : 0][CACHE ? i : 0] : __ldg(Cr + ci), gw[k]);
                 atomicAdd(&sgC[ci], w[k] * g);  // d loss / d C_{a_k} += w_k g
             }
         }
@@ -197,11 +209,11 @@ __global__ void __launch_bounds__(SC_THREADS) sc_epoch_kernel(ScDev p) {
     __syncthreads();
     if (t == 0) {
         float sl = 0.f;
-        for (int i = 0; i < SC_THREADS / 32; i++) sl += sloss[i];
+        for (int i = 0; i < NT / 32; i++) sl += sloss[i];
         p.loss_part[blockIdx.x] = sl;
     }
     float* out = p.partials + (int64_t)blockIdx.x * LD;
-    for (int i = t; i < LD; i += SC_THREADS) out[i] = sgC[i];
+    for (int i = t; i < LD; i += NT) out[i] = sgC[i];
 }
 
 __global__ void sc_codebook_kernel(ScDev p, int nblk) {
@@ -548,11 +560,12 @@ void launch_epoch(scoup_sc* h, const ScDev& p, bool prepare = false) {
     dispatch_dpl(h->D, [&](auto dpl) {
         dispatch_lpl(h->L, [&](auto lpl) {
             dispatch_kmax(h->K, [&](auto km) {
-                auto kern = sc_epoch_kernel<decltype(dpl)::value, decltype(lpl)::value, decltype(km)::value>;
+                constexpr int DPL_ = decltype(dpl)::value, KM_ = decltype(km)::value;
+                auto kern = sc_epoch_kernel<DPL_, decltype(lpl)::value, KM_>;
                 if (prepare)
                     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->epoch_smem);
                 else
-                    kern<<<h->nblk, SC_THREADS, h->epoch_smem, h->stream>>>(p);
+                    kern<<<h->nblk, sc_threads<DPL_, KM_>(), h->epoch_smem, h->stream>>>(p);
             });
         });
     });

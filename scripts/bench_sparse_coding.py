@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Benchmark of SURVEY.md §8(f) NEXT-4: 2D sparse coding (Eq. 4) with the
+paper's recipe (L = 64, K = 4, Adam lr 7e-4, 4,000 epochs, k-means init) on one B200.
+
+Workload: the medium SAM level of BASELINE.json configs[2] ("indoor": 200 views x 128 regions
+= 25,600 regions) with D = 512 synthetic CLIP-like unit features (K-sparse convex combinations
+of a hidden unit codebook plus noise; the paper's CLIP features are not available).  Timed with
+CUDA events: k-means init, the 4,000 epochs, the encode.  The CPU oracle (numpy float64) is
+timed on a few epochs of the same problem and reported per epoch.  Prints one JSON line.
+
+    python scripts/bench_sparse_coding.py [--regions 25600] [--epochs 4000] [--D 512]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--regions", type=int, default=25600)
+    ap.add_argument("--D", type=int, default=512)
+    ap.add_argument("--L", type=int, default=64)
+    ap.add_argument("--K", type=int, default=4)
+    ap.add_argument("--epochs", type=int, default=4000)
+    ap.add_argument("--cpu-epochs", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    from paper_2605_13600_b200 import synth
+    from paper_2605_13600_b200.sparse_coding import SparseCoder
+
+    rf = synth.make_region_features(args.regions, args.D, args.L, args.K, noise=0.05, seed=0)
+    u, E = synth.make_kmeans_draws(args.L, args.D, seed=0)
+    F = torch.from_numpy(rf.F).cuda()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    # warm-up on a copy (module load, graph instantiation paths)
+    w = SparseCoder(F, args.L, args.K)
+    w.kmeans(u, E)
+    w.train(60)
+    w.close()
+    torch.cuda.synchronize()
+    coder = SparseCoder(F, args.L, args.K)
+    s = coder.stream
+    ev[0].record(s)
+    iters = coder.kmeans(u, E)
+    ev[1].record(s)
+    loss = coder.train(args.epochs)
+    ev[2].record(s)
+    atoms, coefs = coder.encode()
+    ev[3].record(s)
+    torch.cuda.synchronize()
+    km_ms, tr_ms, enc_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
+    loss = loss.cpu().numpy()
+    coder.close()
+    # CPU oracle, a few epochs of the same problem from a k-means-free state (per-epoch cost)
+    from oracle import sparse_coding as sc
+    C0 = rf.C_true[np.arange(args.L) % len(rf.C_true)].astype(np.float32)
+    Z0 = sc.init_logits(rf.F, C0).astype(np.float32)
+    st = {"Z": Z0, "C": C0, "mZ": np.zeros_like(Z0), "vZ": np.zeros_like(Z0), "mC": np.zeros_like(C0),
+          "vC": np.zeros_like(C0), "t": 0}
+    t0 = time.perf_counter()
+    for _ in range(args.cpu_epochs):
+        new, _ = sc.epoch(st, rf.F, args.K, sc.AdamHyper())
+        st = {k: (v.astype(np.float32) if isinstance(v, np.ndarray) else v) for k, v in new.items()}
+    cpu_epoch_s = (time.perf_counter() - t0) / args.cpu_epochs
+    # per epoch: the features are read once, the codebook-gradient partials written and summed
+    bytes_epoch = 4.0 * args.regions * args.D + 2 * 4.0 * 148 * args.L * args.D
+    print(json.dumps({
+        "metric": "Eq. 4 sparse coding: seconds per semantic level (k-means + 4,000 Adam epochs + encode)",
+        "value": (km_ms + tr_ms + enc_ms) / 1e3, "unit": "s", "higher_is_better": False,
+        "config": {"workload": f"indoor medium level: R={args.regions} regions, D={args.D}, L={args.L}, "
+                               f"K={args.K}, {args.epochs} epochs", "data": "synthetic CLIP-like unit features"},
+        "kmeans_ms": km_ms, "lloyd_iterations": iters, "train_ms": tr_ms, "epoch_us": 1e3 * tr_ms / args.epochs,
+        "encode_ms": enc_ms, "loss_first": float(loss[0]), "loss_last": float(loss[-1]),
+        "epoch_min_hbm_gbs": bytes_epoch / (tr_ms / args.epochs * 1e-3) / 1e9,
+        "cpu_baseline": {"kind": "oracle", "cores": 1, "sample": f"{args.cpu_epochs} epochs of the same problem",
+                         "epoch_s": cpu_epoch_s, "level_s_extrapolated": cpu_epoch_s * args.epochs},
+        "paper": "sparse coding is ~80% of SCOUP's reconstruction time on an RTX A6000 (P:458)",
+    }))
+
+
+if __name__ == "__main__":
+    main()
