@@ -113,8 +113,6 @@ struct Ctx {
     uint64_t* h_total = nullptr;  // entries of the chunk
     int* h_nsel = nullptr;        // selected elements of the far chunk
     CamBatch* h_cams = nullptr;
-    uint32_t* ids_stage = nullptr;
-    size_t ids_cap = 0;
     // the batch in flight
     Step step = ST_IDLE;
     int v0 = 0, nv = 0;
@@ -167,6 +165,12 @@ struct scoup_uplift {
     int bin_shift = 6;                  // bins of 2^bin_shift px squares
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
     cublasHandle_t blas = nullptr;      // decode GEMM (Eq. 8), created on first use
+    // host region maps: the whole call's maps are copied up front on a copy stream, in chunks of
+    // MAX_VB views with one event each, so the PCIe transfer runs ahead of the batches
+    cudaStream_t copy_s = nullptr;
+    std::vector<cudaEvent_t> chunk_ev;
+    uint32_t* ids_all = nullptr;
+    size_t ids_all_cap = 0;
 };
 
 namespace {
@@ -209,7 +213,7 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.code, b.hist, b.thr, b.cams, b.sel, b.nsel, b.skey, b.skey_alt, b.sval, b.sval_sorted,
                     b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.flags, b.live_sat, b.Tstate, b.tile_live, b.ekey, b.eval,
-                    b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp, c.ids_stage};
+                    b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp};
     for (void* p : ptrs) dfree(p, s);
     void* hp[] = {c.h_hist, c.h_thr, c.h_total, c.h_nsel, c.h_cams};
     for (void* p : hp)
@@ -620,6 +624,27 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
             ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
         }
         args.cams = cams.data();
+        if (!ids_on_device && nlev > 0) {
+            // all views' maps (every level) to the device on the copy stream, chunk by chunk
+            if (!h->copy_s) CK(cudaStreamCreateWithFlags(&h->copy_s, cudaStreamNonBlocking));
+            const int nch = (num_views + MAX_VB - 1) / MAX_VB;
+            while ((int)h->chunk_ev.size() < nch) {
+                cudaEvent_t e = nullptr;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                h->chunk_ev.push_back(e);
+            }
+            grow(&h->ids_all, &h->ids_all_cap, (size_t)nlev * num_views * npx, h->stream, 1.0);
+            CK(cudaEventRecord(h->ev_fork, h->stream));  // the buffer (and earlier readers) are done
+            CK(cudaStreamWaitEvent(h->copy_s, h->ev_fork, 0));
+            for (int j = 0; j < nch; j++) {
+                const int v0 = j * MAX_VB, nv = std::min(MAX_VB, num_views - v0);
+                for (int l = 0; l < nlev; l++)
+                    CK(cudaMemcpyAsync(h->ids_all + ((int64_t)l * num_views + v0) * npx,
+                                       region_ids[l] + (int64_t)v0 * npx, sizeof(uint32_t) * npx * nv,
+                                       cudaMemcpyHostToDevice, h->copy_s));
+                CK(cudaEventRecord(h->chunk_ev[j], h->copy_s));
+            }
+        }
         int next = 0;  // first view not yet assigned to a batch
         auto start_batch = [&](Ctx& c) {
             int B = std::min(Bmax, num_views - next);
@@ -634,19 +659,14 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
             c.nv = B;
             c.key_bits = kb;
             next += B;
-            if (!ids_on_device) grow(&c.ids_stage, &c.ids_cap, (size_t)(Bmax * npx * nlev), c.s, 1.0);
+            if (!ids_on_device && nlev > 0)  // this batch's chunks of the up-front copy
+                for (int j = c.v0 / MAX_VB; j <= (c.v0 + c.nv - 1) / MAX_VB; j++)
+                    CK(cudaStreamWaitEvent(c.s, h->chunk_ev[j], 0));
             for (int v = 0; v < c.nv; v++) {
                 const int u = c.v0 + v;
-                for (int l = 0; l < nlev; l++) {
-                    if (ids_on_device) {
-                        c.ids_dev[v][l] = region_ids[l] + (int64_t)u * npx;
-                    } else {
-                        uint32_t* dst = c.ids_stage + ((int64_t)l * Bmax + v) * npx;
-                        CK(cudaMemcpyAsync(dst, region_ids[l] + (int64_t)u * npx, sizeof(uint32_t) * npx,
-                                           cudaMemcpyHostToDevice, c.s));
-                        c.ids_dev[v][l] = dst;
-                    }
-                }
+                for (int l = 0; l < nlev; l++)
+                    c.ids_dev[v][l] = ids_on_device ? region_ids[l] + (int64_t)u * npx
+                                                    : h->ids_all + ((int64_t)l * num_views + u) * npx;
             }
             step_depth(h, c, args);
         };
@@ -671,6 +691,9 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
         for (int i = 0; i < 2; i++) {
             CK(cudaEventRecord(h->ev_join[i], h->ctx[i].s));
             CK(cudaStreamWaitEvent(h->stream, h->ev_join[i], 0));
+        }
+        if (!ids_on_device && nlev > 0) {  // (every chunk was waited on by a batch; this is the last)
+            CK(cudaStreamWaitEvent(h->stream, h->chunk_ev[(num_views - 1) / MAX_VB], 0));
         }
         add_u64<<<1, 1, 0, h->stream>>>(h->d_stats + 0, (unsigned long long)num_views);
         h->kernel_launches += 1;
@@ -1198,7 +1221,13 @@ void scoup_uplift_free(scoup_uplift* h) {
         dfree(h->Z, h->stream);
     }
     if (h->blas) cublasDestroy(h->blas);
+    dfree(h->ids_all, h->stream);
     cudaStreamSynchronize(h->stream);
+    if (h->copy_s) {
+        cudaStreamSynchronize(h->copy_s);
+        cudaStreamDestroy(h->copy_s);
+    }
+    for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
     delete h;
 }
 

@@ -284,13 +284,15 @@ def _band(cam, y0, y1):
     return synth.Camera(cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.width, y1 - y0, cam.world_to_camera)
 
 
-def run_gpu_levels(g, cams, maps_by_level, codes_by_level, L, K):
-    """Fused multi-level uplift (one raster pass for every level) through the C ABI."""
+def run_gpu_levels(g, cams, maps_by_level, codes_by_level, L, K, host_maps=False):
+    """Fused multi-level uplift (one raster pass for every level) through the C ABI (host_maps:
+    the region maps stay host arrays; the library copies them up front on its copy stream)."""
     from paper_2605_13600_b200.uplift import SparseUplift
     V, M = len(cams), len(maps_by_level)
     gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
                             for a in (g.means, g.scales, g.rotations, g.opacities)])
-    ids = [torch.from_numpy(np.ascontiguousarray(m).view(np.int32)).cuda() for m in maps_by_level]
+    ids = [torch.from_numpy(np.ascontiguousarray(m).view(np.int32)) for m in maps_by_level]
+    ids = [i.pin_memory() if host_maps else i.cuda() for i in ids]
     cods = [synth.Codes(torch.from_numpy(np.ascontiguousarray(c.atoms).view(np.int32)).cuda(),
                         torch.from_numpy(np.ascontiguousarray(c.coefs)).cuda(), c.row0, c.num_regions)
             for c in codes_by_level]
@@ -327,6 +329,9 @@ def test_fused_levels_tiny(dev):
     codes = [synth.make_codes(cfg, level=l, seed=7) for l in range(3)]
     oras = [oracle.uplift(scene.gaussians, scene.cameras, maps[l], codes[l], cfg.L, cfg.K) for l in range(3)]
     res = run_gpu_levels(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    assert_levels_parity(res, oras, cfg.K)
+    # host (pinned) maps: chunked up-front copies on the library's copy stream, same results
+    res = run_gpu_levels(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, host_maps=True)
     assert_levels_parity(res, oras, cfg.K)
 
 
