@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (ntiles <= 0) return;
-    static_assert(sizeof(Smem) <= 3 * 1024 * 74, "three CTAs per SM must fit the 227 KB shared memory");
+    static_assert(3 * (sizeof(Smem) + 1024) <= 228 * 1024, "three CTAs per SM must fit the 228 KB shared memory");
     static bool attr_set = false;  // the opt-in above 48 KB of dynamic shared memory, once
     if (!attr_set) {
         cudaFuncSetAttribute(raster_aggregate_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
