@@ -370,6 +370,10 @@ def main():
                        "l2": "inputs larger than L2 (region maps %.2f GB, W %.0f MB per GPU)" % (
                            sum(m.numel() for m in maps_l) * 4 / 1e9, nlev * Npad * L * 4 / 1e6)},
             "contributions_per_step": int(contrib_step),
+            # atom updates = contributions x S per level (every outdoor pixel is
+            # coded; dense mode: x D), and the per-GPU rate
+            "atom_updates_per_s": value * cfg.S * nlev,
+            "contributions_per_s_per_gpu": value / world,
             "support_tests_per_step": int(tests_step),
             "lane_evaluations_per_step": int(lane_evals_step),
             "raster_lane_use": tests_step / max(1, lane_evals_step),
