@@ -39,7 +39,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + BATCH)
 constexpr int NWARP = TILE_PIX / 32;
 #ifndef RGROUP
-#define RGROUP 4                              // records per warp-uniform branch in the pixel loop
+#define RGROUP 8                              // records per warp-uniform branch in the pixel loop (even: pairs)
 #endif
 
 // Sum e[i] over the lanes in the group (all lanes if !MASKED); lane l returns the sum for i = l.
@@ -78,6 +78,59 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// ---- paired FP32 (sm_100 FADD2 / FMUL2 / FFMA2): two independent IEEE round-to-nearest
+// operations per instruction; a pair lives in a 64-bit register (lo = first element)
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 f2_pack(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_split(f2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_sub(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f2 f2_rsub(f2 a, float s) { return f2_sub(f2_pack(s, s), a); }  // s - a
+__device__ __forceinline__ f2 f2_fmac(f2 a, f2 b, float c) { return f2_fma(a, b, f2_pack(c, c)); }
+
+// exp2_spec (internal.cuh) on a pair: the same operations element-wise.
+__device__ __forceinline__ f2 exp2_spec2(f2 y) {
+    const float magic = 0x1.8p23f;  // 1.5 * 2^23
+    const f2 mg = f2_pack(magic, magic);
+    const f2 t = f2_add(y, mg);
+    const f2 kf = f2_sub(t, mg);
+    const f2 f = f2_sub(y, kf);
+    f2 p = f2_fmac(f2_pack(0x1.5bba14p-10f, 0x1.5bba14p-10f), f, 0x1.3cea88p-7f);
+    p = f2_fmac(p, f, 0x1.c6b752p-5f);
+    p = f2_fmac(p, f, 0x1.ebf9bcp-3f);
+    p = f2_fmac(p, f, 0x1.62e42ap-1f);
+    p = f2_fmac(p, f, 1.0f);
+    float p0, p1, t0, t1;
+    f2_split(p, p0, p1);
+    f2_split(t, t0, t1);
+    return f2_pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                   __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 // Fallback aggregation of one fragment: every level's code of the pixel (row < 0: unassigned at
 // that level, no W), and Z.  Scalars only, so the call needs no local-memory copies.
 __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* atoms, const float* coefs, int S,
@@ -96,12 +149,19 @@ __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* a
 }
 
 static_assert(BATCH == 32, "batch = one record per lane (transpose-reduction, flush indexing)");
+static_assert(RGROUP % 2 == 0 && BATCH % RGROUP == 0, "records are evaluated in pairs");
 
 struct Ring {
     // ring of candidate records; slots [0, BATCH) are mirrored at [QCAP, QCAP + BATCH) so a
     // batch q_head .. q_head + BATCH - 1 is always contiguous
-    float4 q0[QCAP + BATCH];     // (mx, my, r, o)
-    float4 q1[QCAP + BATCH];     // (qa, qb, qc, ycut)
+    // (mx, my, r, o) and (qa, qb, qc, ycut) of records 2i and 2i+1, pair-interleaved so the
+    // pixel loop evaluates two records per paired-FP32 instruction (FADD2 / FMUL2 / FFMA2):
+    // p0[i] = (mx, mx', my, my'), p1[i] = (r, r', o, o'), p2[i] = (qa, qa', qb, qb'),
+    // p3[i] = (qc, qc', ycut, ycut')
+    float4 p0[(QCAP + BATCH) / 2];
+    float4 p1[(QCAP + BATCH) / 2];
+    float4 p2[(QCAP + BATCH) / 2];
+    float4 p3[(QCAP + BATCH) / 2];
     float4 q2[QCAP + BATCH];     // (support-box half-extents x, y, Gaussian id, sy)
     float4 q3[QCAP + BATCH];     // band_relevant parameters
 };
@@ -164,8 +224,20 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         return;
     }
     const int nlev = NLEV1 ? 1 : p.nlev;
-    float4* const q0 = sm.u.r.q0;
-    float4* const q1 = sm.u.r.q1;
+    float* const pf0 = reinterpret_cast<float*>(sm.u.r.p0);
+    float* const pf1 = reinterpret_cast<float*>(sm.u.r.p1);
+    float* const pf2 = reinterpret_cast<float*>(sm.u.r.p2);
+    float* const pf3 = reinterpret_cast<float*>(sm.u.r.p3);
+    // record at ring position pos: element (pos >> 1) * 4 + (pos & 1) (+ 2 for the second pair)
+    auto put_pair_rec = [&](uint32_t pos, const float4& r0, const float4& r1) {
+        const uint32_t b = (pos >> 1) * 4 + (pos & 1);
+        pf0[b] = r0.x; pf0[b + 2] = r0.y; pf1[b] = r0.z; pf1[b + 2] = r0.w;
+        pf2[b] = r1.x; pf2[b + 2] = r1.y; pf3[b] = r1.z; pf3[b + 2] = r1.w;
+    };
+    auto get_rec0 = [&](uint32_t pos) {
+        const uint32_t b = (pos >> 1) * 4 + (pos & 1);
+        return make_float4(pf0[b], pf0[b + 2], pf1[b], pf1[b + 2]);
+    };
     float4* const q2 = sm.u.r.q2;
     float4* const q3 = sm.u.r.q3;
     // pixel-centre rectangles of the tile and of this warp's 8x4 block (clipped to the image)
@@ -319,13 +391,11 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             }
             if (acc) {
                 const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
-                q0[pos] = r0;
-                q1[pos] = r1;
+                put_pair_rec(pos, r0, r1);
                 q2[pos] = r2;
                 q3[pos] = r3;
                 if (pos < (uint32_t)BATCH) {
-                    q0[pos + QCAP] = r0;
-                    q1[pos + QCAP] = r1;
+                    put_pair_rec(pos + QCAP, r0, r1);
                     q2[pos + QCAP] = r2;
                     q3[pos + QCAP] = r3;
                 }
@@ -336,12 +406,22 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         }
         if (q_count == 0) break;
         const uint32_t n = min((uint32_t)BATCH, q_count);
+        if (n < (uint32_t)BATCH) {
+            // the tile's last, partial batch: the ring slots past it hold stale records, which
+            // the pixel loop (it evaluates whole record groups without a per-record mask test)
+            // must see as empty -- a negative support radius fails every square test
+            if ((uint32_t)t >= n && t < BATCH) {
+                const uint32_t pos = q_head + (uint32_t)t;
+                pf1[(pos >> 1) * 4 + (pos & 1)] = -1.0f;
+            }
+            __syncthreads();
+        }
 
         // ---- per-warp mask of batch records that may touch this warp's 8x4 block
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
         if (!warp_done && (uint32_t)lane < n)
-            rel = band_relevant(q0[q_head + lane], q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
+            rel = band_relevant(get_rec0(q_head + lane), q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
         const unsigned mask = __ballot_sync(FULL, rel);
 
         // ---- rasterise: e[j] for batch record j, in depth order (DESIGN.md §3 PX).
@@ -351,36 +431,54 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         // mask is a no-op (its `sq` is false).
         float e[BATCH];
         uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
-        const float4* b0 = q0 + q_head;
-        const float4* b1 = q1 + q_head;
+        // batches start at even ring positions (q_head is a multiple of BATCH until the last)
+        const ulonglong2* b0 = reinterpret_cast<const ulonglong2*>(sm.u.r.p0) + (q_head >> 1);
+        const ulonglong2* b1 = reinterpret_cast<const ulonglong2*>(sm.u.r.p1) + (q_head >> 1);
+        const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(sm.u.r.p2) + (q_head >> 1);
+        const ulonglong2* b3 = reinterpret_cast<const ulonglong2*>(sm.u.r.p3) + (q_head >> 1);
 #pragma unroll
         for (int j = 0; j < BATCH; j++) e[j] = 0.f;
 #pragma unroll
         for (int g0 = 0; g0 < BATCH; g0 += RGROUP)
         if ((mask >> g0) & ((1u << RGROUP) - 1u)) {
 #pragma unroll
-        for (int j = g0; j < g0 + RGROUP; j++) {
-            {
-                const float4 a = b0[j];  // mx, my, r, o
-                const float4 b = b1[j];  // qa, qb, qc, ycut
-                const float dx = __fsub_rn(px, a.x), dy = __fsub_rn(py, a.y);
+        for (int j = g0; j < g0 + RGROUP; j += 2) {
+            // T-independent part of records j and j+1 in paired FP32 (each half is the exact
+            // DESIGN.md §3 scalar operation, round-to-nearest, no contraction)
+            const ulonglong2 A0 = b0[j >> 1], A1 = b1[j >> 1], A2 = b2[j >> 1], A3 = b3[j >> 1];
+            const f2 dx = f2_rsub(A0.x, px), dy = f2_rsub(A0.y, py);      // px - mx, py - my
+            const f2 q = f2_fma(dx, f2_fma(A2.x, dx, f2_mul(A2.y, dy)), f2_mul(f2_mul(A3.x, dy), dy));
+            const f2 ex = exp2_spec2(q);
+            float mx_lo, mx_hi;
+            f2_split(f2_mul(A1.y, ex), mx_lo, mx_hi);                       // o * exp2_spec(q)
+            const float al0 = fminf(K_ACLAMP, mx_lo), al1 = fminf(K_ACLAMP, mx_hi);
+            float om0, om1;
+            f2_split(f2_rsub(f2_pack(al0, al1), 1.0f), om0, om1);            // 1 - alpha
+            float dx0, dx1, dy0, dy1, q0, q1, r0, r1, y0, y1;
+            f2_split(dx, dx0, dx1);
+            f2_split(dy, dy0, dy1);
+            f2_split(q, q0, q1);
+            f2_split(A1.x, r0, r1);
+            f2_split(A3.y, y0, y1);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const float dxh = h ? dx1 : dx0, dyh = h ? dy1 : dy0, qh = h ? q1 : q0, rh = h ? r1 : r0;
+                const float yh = h ? y1 : y0, al = h ? al1 : al0, om = h ? om1 : om0;
+                const int jj = j + h;
                 // (a finished pixel, T == 0, needs no test of its own: its Tn = 0 < 1e-4 makes
                 // every later fragment a non-contributing stop that leaves T = 0)
                 // (the record's warp-mask bit is only needed for the support-test count: a
                 // record outside the mask cannot pass the alpha test anywhere in the block --
                 // band_relevant is conservative -- so it is a no-op for every lane)
-                const bool sq = (!COUNT || ((mask >> j) & 1u)) && fabsf(dx) <= a.z && fabsf(dy) <= a.z;
+                const bool sq = (!COUNT || ((mask >> jj) & 1u)) && fabsf(dxh) <= rh && fabsf(dyh) <= rh;
                 const bool active = COUNT && T > 0.f;
-                const float q = __fmaf_rn(dx, __fmaf_rn(b.x, dx, __fmul_rn(b.y, dy)),
-                                          __fmul_rn(__fmul_rn(b.z, dy), dy));
-                const float al = fminf(K_ACLAMP, __fmul_rn(a.w, exp2_spec(q)));
-                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
-                const bool pass = sq && !(q > 0.f) && q >= b.w && al >= K_AMIN;
+                const float Tn = __fmul_rn(T, om);
+                const bool pass = sq && !(qh > 0.f) && qh >= yh && al >= K_AMIN;
                 const bool con = pass && !(Tn < K_TMIN);
-                e[j] = con ? __fmul_rn(al, T) : 0.f;
+                e[jj] = con ? __fmul_rn(al, T) : 0.f;
                 T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
-                if (COUNT && con) cbits |= 1u << j;
-                if (COUNT && sq && active) tbits |= 1u << j;
+                if (COUNT && con) cbits |= 1u << jj;
+                if (COUNT && sq && active) tbits |= 1u << jj;
             }
         }
         }
