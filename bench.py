@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dense", type=int, default=0,
                     help="dense feature uplift baseline (Eq. 3) with D-dim region features instead of codes")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: fused peer-read reduction + Top-K over CUDA IPC (default), or NCCL "
+                         "reduce-scatter + Top-K")
     return ap.parse_args()
 
 
@@ -236,11 +239,29 @@ def main():
         else:
             u.add_views(cams, m_l, c_l)
 
+    # N > 1: the fused exchange reads the peers' accumulators through CUDA IPC mappings (set up
+    # once for the timed handle); if the mappings cannot be made, NCCL reduce-scatter is used
+    peers, peer_bases, exchange = None, [], "nccl" if world == 1 else args.exchange
+    if world > 1 and exchange == "fused" and not dense:
+        try:
+            peers, peer_bases = D.exchange_accumulators(up.W, rank, world, local)
+        except Exception as ex:  # noqa: BLE001 -- reported, then the NCCL path
+            print(f"[rank {rank}] fused exchange unavailable ({ex}); using NCCL reduce-scatter", file=sys.stderr)
+            exchange = "nccl"
+        flags = [exchange == "fused"] * 1
+        allf = [None] * world
+        dist.all_gather_object(allf, flags[0])
+        if not all(allf):
+            exchange = "nccl"
+
     def finalize_all(u, out_atoms=None, out_coefs=None):
         if dense:  # Eq. 3 needs no Top-K: f_i = W_i / Z_i (W is the output)
             return
         for lvl in range(nlev):
-            if world > 1:
+            if world > 1 and u is up and exchange == "fused":
+                D.fused_reduce_finalize(u, peers, first_row, shard, level=lvl, out_atoms=out_atoms,
+                                        out_coefs=out_coefs)
+            elif world > 1:
                 Wl = u.W if nlev == 1 else u.W[lvl]
                 D.reduce_scatter_accumulators(Wl, u.Z, Ws, Zs)
                 u.finalize(first_row=first_row, num_rows=shard, W_rows=Ws, Z_rows=Zs, level=lvl,
@@ -366,7 +387,8 @@ def main():
             "config": {"workload": cfg.name + (f"-dense{L}" if dense else ""), "gaussians": G, "views": cfg.num_views, "width": cfg.width,
                        "height": cfg.height, "L": L, "S": cfg.S, "K": K, "levels": nlev,
                        "regions_per_view": list(cfg.regions),
-                       "parallelism": f"view-sharded x{world} + reduce-scatter" if world > 1 else "single GPU",
+                       "parallelism": (f"view-sharded x{world} + " + ("fused peer-read reduction + Top-K (CUDA IPC)"
+                                       if exchange == "fused" else "NCCL reduce-scatter")) if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (region maps %.2f GB, W %.0f MB per GPU)" % (
                            sum(m.numel() for m in maps_l) * 4 / 1e9, nlev * Npad * L * 4 / 1e6)},
             "contributions_per_step": int(contrib_step),
@@ -393,6 +415,11 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if peer_bases:  # every rank has finished reading every accumulator (the finalize barriers)
+        from paper_2605_13600_b200 import abi
+        barrier()
+        for b in peer_bases:
+            abi.scoup_ipc_close(local, b)
     up.close()
     if world > 1:
         dist.destroy_process_group()

@@ -219,6 +219,37 @@ scoup_status scoup_uplift_finalize_topk_level(scoup_uplift *h, int32_t level, in
                                               const float *W_rows, const float *Z_rows, uint32_t *out_atoms,
                                               float *out_coefs);
 
+/*
+ * Fused cross-rank reduction + Top-K (Eq. 5 is a sum over views, so
+ * the ranks' view-sharded partials add; Eq. 6, on the sum).  Rows [first_row,
+ * first_row + num_rows) of level `level`: W = sum over q < num_peers of W_peers[q] (summed in
+ * rank order 0..P-1, fp32), then Top-K + L1 renormalisation exactly as
+ * scoup_uplift_finalize_topk.  W_peers: host array of num_peers (<= 16) device-accessible
+ * pointers to each rank's accumulator base (the W of scoup_uplift_init, [levels][rows_padded][L],
+ * same layout on every rank): the local one and the others' CUDA IPC mappings
+ * (scoup_ipc_import); 16-byte aligned; L % 4 == 0.  This replaces the reduce-scatter + finalize
+ * pair: the shard's rows are read once, directly from the peers' memory over NVLink, and no
+ * reduced shard is written.  The caller must ensure every peer's accumulation is complete
+ * before the call and that no peer modifies or frees its W until every rank has returned
+ * (e.g. a barrier on each side).  Outputs are device memory.  Synchronising.  Errors: EINVAL,
+ * EUNSUPPORTED (L % 4 != 0), ECUDA.
+ */
+scoup_status scoup_uplift_finalize_topk_peers(scoup_uplift *h, int32_t level, int64_t first_row, int64_t num_rows,
+                                              int32_t num_peers, const float *const *W_peers, uint32_t *out_atoms,
+                                              float *out_coefs);
+
+/*
+ * CUDA IPC plumbing for scoup_uplift_finalize_topk_peers: export a device pointer as an
+ * allocation handle (SCOUP_IPC_HANDLE_BYTES opaque bytes) plus the pointer's offset inside that
+ * allocation; import a peer's handle on `device` (peer access enabled lazily) -> the mapped
+ * pointer and the mapping's base; close a mapping by its base.  The allocation must come from
+ * cudaMalloc (e.g. the PyTorch caching allocator), not from a stream-ordered pool.
+ */
+#define SCOUP_IPC_HANDLE_BYTES 64
+scoup_status scoup_ipc_export(const void *dptr, void *handle_out, int64_t *offset_out);
+scoup_status scoup_ipc_import(int device, const void *handle, int64_t offset, void **dptr_out, void **base_out);
+scoup_status scoup_ipc_close(int device, void *base);
+
 /* Zero the accumulators and counters and clear a latched error (stream-ordered). */
 scoup_status scoup_uplift_reset(scoup_uplift *h);
 

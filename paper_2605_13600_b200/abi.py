@@ -45,7 +45,8 @@ class scoup_timing(C.Structure):
 
 EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
            "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
-           "scoup_uplift_render_views", "scoup_uplift_decode",
+           "scoup_uplift_render_views", "scoup_uplift_decode", "scoup_uplift_finalize_topk_peers",
+           "scoup_ipc_export", "scoup_ipc_import", "scoup_ipc_close",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
            "scoup_uplift_free", "scoup_last_error", "scoup_version",
@@ -81,6 +82,10 @@ def lib():
         L.scoup_uplift_free.argtypes = [P]
         L.scoup_uplift_free.restype = None
         L.scoup_last_error.restype = C.c_char_p
+        L.scoup_uplift_finalize_topk_peers.argtypes = [P, i32, i64, i64, i32, P, P, P]
+        L.scoup_ipc_export.argtypes = [P, P, C.POINTER(i64)]
+        L.scoup_ipc_import.argtypes = [C.c_int, P, i64, C.POINTER(P), C.POINTER(P)]
+        L.scoup_ipc_close.argtypes = [C.c_int, P]
         L.scoup_sc_init.argtypes = [C.c_int, P, i64, i32, i32, i32, P, C.POINTER(P)]
         L.scoup_sc_kmeans.argtypes = [P, P, P, i32, C.POINTER(i32)]
         L.scoup_sc_set_state.argtypes = [P, P, P, P, P, P, P, i64]
@@ -281,3 +286,35 @@ def scoup_sc_encode(h: int, atoms, coefs) -> None:
 def scoup_sc_free(h: int) -> None:
     if h:
         lib().scoup_sc_free(h)
+
+
+# ---- fused cross-rank reduction + Top-K and its CUDA IPC plumbing (include/scoup.h) ------------
+
+IPC_HANDLE_BYTES = 64
+
+
+def scoup_uplift_finalize_topk_peers(h: int, level: int, first_row: int, num_rows: int, W_peers: Sequence[int],
+                                     out_atoms, out_coefs) -> None:
+    arr = (C.c_void_p * len(W_peers))(*W_peers)
+    _check(lib().scoup_uplift_finalize_topk_peers(h, level, first_row, num_rows, len(W_peers), arr, ptr(out_atoms),
+                                                  ptr(out_coefs)))
+
+
+def scoup_ipc_export(dptr: int):
+    """-> (handle bytes, offset of dptr inside its allocation)."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    off = C.c_int64(0)
+    _check(lib().scoup_ipc_export(dptr, buf, C.byref(off)))
+    return bytes(buf.raw), off.value
+
+
+def scoup_ipc_import(device: int, handle: bytes, offset: int):
+    """-> (mapped pointer, mapping base for scoup_ipc_close)."""
+    buf = C.create_string_buffer(handle, IPC_HANDLE_BYTES)
+    d, b = C.c_void_p(), C.c_void_p()
+    _check(lib().scoup_ipc_import(device, buf, offset, C.byref(d), C.byref(b)))
+    return d.value, b.value
+
+
+def scoup_ipc_close(device: int, base: int) -> None:
+    _check(lib().scoup_ipc_close(device, base))

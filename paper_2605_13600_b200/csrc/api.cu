@@ -11,6 +11,7 @@
 // the GPU runs view v-1's raster.
 // finalize_topk runs Eq. 6 on the requested rows.
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
@@ -1108,6 +1109,89 @@ scoup_status scoup_uplift_finalize_topk_level(scoup_uplift* h, int32_t level, in
     } catch (const CudaError& e) {
         return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
     }
+}
+
+scoup_status scoup_uplift_finalize_topk_peers(scoup_uplift* h, int32_t level, int64_t first_row, int64_t num_rows,
+                                              int32_t num_peers, const float* const* W_peers, uint32_t* out_atoms,
+                                              float* out_coefs) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (first_row < 0 || num_rows < 0 || first_row + num_rows > h->Npad)
+        return fail(SCOUP_EINVAL, "row range outside [0, rows_padded)");
+    if (level < 0 || level >= h->nlev) return fail(SCOUP_EINVAL, "level out of range");
+    if (num_peers < 1 || num_peers > MAX_PEERS) return fail(SCOUP_EINVAL, "num_peers outside [1, 16]");
+    if (!W_peers) return fail(SCOUP_EINVAL, "W_peers is NULL");
+    if (num_rows > 0 && (!out_atoms || !out_coefs)) return fail(SCOUP_EINVAL, "NULL output");
+    if (h->L % 4 != 0) return fail(SCOUP_EUNSUPPORTED, "peer reduction needs L % 4 == 0");
+    PeerRows pr{};
+    pr.n = num_peers;
+    for (int q = 0; q < num_peers; q++) {
+        if (!W_peers[q] || (reinterpret_cast<uintptr_t>(W_peers[q]) & 15))
+            return fail(SCOUP_EINVAL, "peer accumulator " + std::to_string(q) + " NULL or not 16-byte aligned");
+        pr.W[q] = W_peers[q] + (int64_t)level * h->Npad * h->L;
+    }
+    try {
+        DeviceGuard dg(h->device);
+        if (num_rows > 0) {
+            if (!is_device_ptr(out_atoms) || !is_device_ptr(out_coefs))
+                return fail(SCOUP_EINVAL, "peer finalize writes device outputs");
+            const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(num_rows, h->G - first_row));
+            launch_topk_peers(pr, first_row, num_rows, valid, h->L, h->K, out_atoms, out_coefs, h->stream);
+            h->kernel_launches += 1;
+            CK(cudaGetLastError());
+        }
+        CK(cudaStreamSynchronize(h->stream));
+        return check_latched(h);
+    } catch (const CudaError& e) {
+        return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
+    }
+}
+
+scoup_status scoup_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out) {
+    g_last_error.clear();
+    if (!dptr || !handle_out || !offset_out) return fail(SCOUP_EINVAL, "NULL argument");
+    static CUresult (*range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+    if (!range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(SCOUP_ECUDA, "cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+        return fail(SCOUP_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t hd;
+    const cudaError_t e = cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return fail(SCOUP_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    static_assert(sizeof(cudaIpcMemHandle_t) == SCOUP_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &hd, sizeof(hd));
+    *offset_out = (int64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    return SCOUP_OK;
+}
+
+scoup_status scoup_ipc_import(int device, const void* handle, int64_t offset, void** dptr_out, void** base_out) {
+    g_last_error.clear();
+    if (!handle || !dptr_out || !base_out || offset < 0) return fail(SCOUP_EINVAL, "bad argument");
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    void* base = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(SCOUP_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    *base_out = base;
+    *dptr_out = static_cast<char*>(base) + offset;
+    return SCOUP_OK;
+}
+
+scoup_status scoup_ipc_close(int device, void* base) {
+    g_last_error.clear();
+    if (!base) return SCOUP_OK;
+    DeviceGuard dg(device);
+    const cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) return fail(SCOUP_ECUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+    return SCOUP_OK;
 }
 
 scoup_status scoup_uplift_reset(scoup_uplift* h) {

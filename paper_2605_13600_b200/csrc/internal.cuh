@@ -298,6 +298,16 @@ __device__ __forceinline__ float pixel_fragment(const float4& a, const float4& b
     return e;
 }
 
+// fused cross-rank reduction + Top-K (kernels.cu): the P ranks' partial W (this level's base,
+// [Npad, L] each), device-accessible pointers (local or CUDA IPC mappings)
+constexpr int MAX_PEERS = 16;
+struct PeerRows {
+    const float* W[MAX_PEERS];
+    int n;
+};
+void launch_topk_peers(const PeerRows& peers, int64_t first_row, int64_t rows, int64_t valid_rows, int L, int K,
+                       uint32_t* atoms, float* coefs, cudaStream_t s);
+
 // thread-local message returned by scoup_last_error() (api.cu)
 void set_last_error(const char* msg);
 

@@ -706,6 +706,76 @@ void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_
                                                             coefs_out, err);
 }
 
+// Fused cross-rank reduction + Top-K (SURVEY.md §8(e)'s fusion option): the rows of this rank's
+// shard are summed over the P ranks' partial accumulators in place -- read directly from the
+// peers' memory (CUDA IPC mappings over NVLink / NVSwitch), in rank order 0..P-1 -- and Eq. 6
+// runs on the sums in registers.  This replaces reduce-scatter + Top-K: no reduced shard is
+// written and re-read.  One thread per row; float4 loads of each peer's row.
+template <int KMAX>
+__global__ void __launch_bounds__(128) topk_peers_kernel(PeerRows peers, int64_t first_row, int64_t rows,
+                                                         int64_t valid_rows, int L, int K,
+                                                         uint32_t* __restrict__ atoms, float* __restrict__ coefs) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float bv[KMAX];
+    uint32_t ba[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
+    if (r < valid_rows) {
+        const int64_t off = (first_row + r) * (int64_t)L;
+        for (int c4 = 0; c4 < L / 4; c4++) {
+            float4 v4 = __ldg(reinterpret_cast<const float4*>(peers.W[0] + off) + c4);
+            for (int q = 1; q < peers.n; q++) {
+                const float4 w4 = __ldg(reinterpret_cast<const float4*>(peers.W[q] + off) + c4);
+                v4.x = __fadd_rn(v4.x, w4.x);
+                v4.y = __fadd_rn(v4.y, w4.y);
+                v4.z = __fadd_rn(v4.z, w4.z);
+                v4.w = __fadd_rn(v4.w, w4.w);
+            }
+            float vals[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                float v = vals[u];
+                if (v > bv[KMAX - 1]) {
+                    uint32_t a = (uint32_t)(c4 * 4 + u);
+#pragma unroll
+                    for (int s = 0; s < KMAX; s++) {
+                        bool sw = v > bv[s];
+                        float tv = sw ? bv[s] : v;
+                        uint32_t ta = sw ? ba[s] : a;
+                        bv[s] = sw ? v : bv[s];
+                        ba[s] = sw ? a : ba[s];
+                        v = tv;
+                        a = ta;
+                    }
+                }
+            }
+        }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int s = 0; s < KMAX; s++)
+        if (s < K) sum = __fadd_rn(sum, bv[s]);
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) {
+        if (s < K) {
+            bool keep = bv[s] > 0.f;
+            atoms[r * K + s] = keep ? ba[s] : NONE;
+            coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+        }
+    }
+}
+
+void launch_topk_peers(const PeerRows& peers, int64_t first_row, int64_t rows, int64_t valid_rows, int L, int K,
+                       uint32_t* atoms, float* coefs, cudaStream_t s) {
+    if (rows <= 0) return;
+    const unsigned g = grid_for(rows, 128);
+    if (K <= 4) topk_peers_kernel<4><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
+    else if (K <= 8) topk_peers_kernel<8><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
+    else if (K <= 16) topk_peers_kernel<16><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
+    else topk_peers_kernel<32><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
+}
+
 template <int KMAX>
 static void topk_dispatch(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
                           float* coefs, cudaStream_t s) {

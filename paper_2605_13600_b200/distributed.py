@@ -51,6 +51,49 @@ def all_gather_codes(atoms_shard, coefs_shard, atoms_all, coefs_all, group=None)
     dist.all_gather_into_tensor(coefs_all, coefs_shard, group=group)
 
 
+def exchange_accumulators(W, rank: int, world: int, device: int, group=None, abi_mod=None):
+    """Share every rank's accumulator with every other rank through CUDA IPC (NVLink / NVSwitch
+    peer mappings): export the local W's allocation handle, all-gather (handle, offset) over the
+    process group, open the peers' handles.  Returns (pointers in rank order, mapping bases to
+    close); pointer `rank` is the local one."""
+    import torch.distributed as dist
+    if abi_mod is None:
+        from . import abi as abi_mod
+    local = W.data_ptr()
+    mine = abi_mod.scoup_ipc_export(local)
+    every = [None] * world
+    dist.all_gather_object(every, mine, group=group)
+    ptrs, bases = [], []
+    for q, (handle, off) in enumerate(every):
+        if q == rank:
+            ptrs.append(local)
+            continue
+        p, b = abi_mod.scoup_ipc_import(device, handle, off)
+        ptrs.append(p)
+        bases.append(b)
+    return ptrs, bases
+
+
+def fused_reduce_finalize(up, peers, first_row: int, num_rows: int, level: int = 0, out_atoms=None,
+                          out_coefs=None, group=None):
+    """SURVEY.md §8(e)'s fused exchange: after a barrier (every rank's partial is complete), one
+    kernel reads this rank's rows from all P partials over the peer mappings, sums them in rank
+    order and runs Eq. 6 -- no reduced shard is written; a second barrier keeps the peers' W
+    alive until every rank has read it."""
+    import torch
+    import torch.distributed as dist
+    from . import abi
+    if out_atoms is None:
+        out_atoms = torch.empty((num_rows, up.K), dtype=torch.int32, device=up.device)
+    if out_coefs is None:
+        out_coefs = torch.empty((num_rows, up.K), dtype=torch.float32, device=up.device)
+    up.stream.synchronize()
+    dist.barrier(group=group)
+    abi.scoup_uplift_finalize_topk_peers(up._h, level, first_row, num_rows, peers, out_atoms, out_coefs)
+    dist.barrier(group=group)
+    return out_atoms, out_coefs
+
+
 class ShardedUplift:
     """One rank of a view-sharded uplift of one semantic level.
 

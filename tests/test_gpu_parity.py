@@ -572,3 +572,48 @@ def test_decode_matches_fp64(dev, L, D, P):
     bound = 1e-5 * (np.abs(W.astype(np.float64)) @ np.abs(C.astype(np.float64))) + 1e-30
     err = np.abs(got - ref)
     assert (err <= bound).all(), (int((err > bound).sum()), float((err / bound).max()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_peer_reduce_topk_matches_oracle(dev, tiny_scene, world):
+    """SURVEY.md §8(e) fused exchange, with the ranks emulated as `world` accumulators on one GPU
+    (one kernel reads every rank's data, as the ranks' kernels would over NVLink): each rank
+    accumulates the views v = r (mod P) into its own W; finalize_topk_peers then sums each rank's
+    row shard over all partials and runs Eq. 6.  The concatenated shard codes equal the oracle's
+    codes of the whole view set (Top-K comparator, fp32 reassociation only)."""
+    from helpers import compare_codes
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200 import distributed as D
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    g = scene.gaussians
+    Wo = oracle.uplift(g, scene.cameras, maps, codes, cfg.L, cfg.K)[0]
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    Npad = D.padded_rows(g.count, world)
+    ups = [SparseUplift(gin, cfg.L, cfg.K, rows_padded=Npad) for _ in range(world)]
+    try:
+        ids = torch.from_numpy(np.ascontiguousarray(maps).view(np.int32)).cuda()
+        for r, up in enumerate(ups):
+            vs = D.views_for_rank(len(scene.cameras), r, world)
+            sub = synth.Codes(torch.from_numpy(np.ascontiguousarray(codes.atoms).view(np.int32)).cuda(),
+                              torch.from_numpy(np.ascontiguousarray(codes.coefs)).cuda(),
+                              np.ascontiguousarray(codes.row0[vs]), np.ascontiguousarray(codes.num_regions[vs]))
+            up.add_views([scene.cameras[v] for v in vs], ids[vs].contiguous(), sub)
+        torch.cuda.synchronize()
+        peers = [up.W.data_ptr() for up in ups]
+        atoms, coefs = [], []
+        for r, up in enumerate(ups):
+            first, n = D.row_shard(g.count, r, world)
+            a = torch.empty((n, cfg.K), dtype=torch.int32, device="cuda")
+            c = torch.empty((n, cfg.K), dtype=torch.float32, device="cuda")
+            abi.scoup_uplift_finalize_topk_peers(up._h, 0, first, n, peers, a, c)
+            atoms.append(a.cpu().numpy())
+            coefs.append(c.cpu().numpy())
+    finally:
+        for up in ups:
+            up.close()
+    A = np.concatenate(atoms)[:g.count].view(np.uint32)
+    Cc = np.concatenate(coefs)[:g.count]
+    bad, ties, worst = compare_codes(A, Cc, Wo, cfg.K)
+    assert bad == 0, worst

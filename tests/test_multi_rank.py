@@ -101,3 +101,56 @@ def _worker(rank, world, port, result_dir):
 def test_gloo_view_sharded_reduce_scatter_matches_single_process(world, tmp_path):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     assert sorted(os.listdir(tmp_path)) == [f"ok{r}" for r in range(world)]
+
+
+class _FakeW:
+    def __init__(self, p):
+        self._p = p
+
+    def data_ptr(self):
+        return self._p
+
+
+class _FakeAbi:
+    """Stands in for the CUDA IPC calls: rank q's handle encodes q; importing it 'maps' it at
+    0x1000 * (q + 1) + offset."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = []
+
+    def scoup_ipc_export(self, dptr):
+        return bytes([self.rank]) * 64, 16 * (self.rank + 1)
+
+    def scoup_ipc_import(self, device, handle, offset):
+        q = handle[0]
+        assert handle == bytes([q]) * 64 and q != self.rank and offset == 16 * (q + 1)
+        self.opened.append(q)
+        return 0x1000 * (q + 1) + offset, 0x1000 * (q + 1)
+
+
+def _exchange_worker(rank, world, port, result_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fake = _FakeAbi(rank)
+        ptrs, bases = D.exchange_accumulators(_FakeW(0xABC0 + rank), rank, world, device=0, abi_mod=fake)
+        expect = [0xABC0 + q if q == rank else 0x1000 * (q + 1) + 16 * (q + 1) for q in range(world)]
+        ok = ptrs == expect and sorted(fake.opened) == [q for q in range(world) if q != rank] and \
+            bases == [0x1000 * (q + 1) for q in range(world) if q != rank]
+        with open(os.path.join(result_dir, f"ex{rank}.txt"), "w") as fh:
+            fh.write("ok" if ok else f"bad {ptrs} {bases}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_accumulator_exchange_over_gloo(tmp_path, world):
+    """The host side of the fused cross-rank reduction (distributed.exchange_accumulators): every
+    rank ends with one pointer per rank in rank order -- its own W and the peers' IPC mappings --
+    and opens exactly the other ranks' handles (CUDA IPC calls replaced by a recording fake)."""
+    mp.spawn(_exchange_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert open(os.path.join(tmp_path, f"ex{r}.txt")).read() == "ok"
