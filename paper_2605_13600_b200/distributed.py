@@ -60,9 +60,14 @@ def exchange_accumulators(W, rank: int, world: int, device: int, group=None, abi
     if abi_mod is None:
         from . import abi as abi_mod
     local = W.data_ptr()
-    mine = abi_mod.scoup_ipc_export(local)
+    try:
+        mine = abi_mod.scoup_ipc_export(local)
+    except Exception:  # still join the collective, so that no rank waits for this one
+        mine = None
     every = [None] * world
     dist.all_gather_object(every, mine, group=group)
+    if any(x is None for x in every):
+        raise RuntimeError("a rank could not export its accumulator for CUDA IPC")
     ptrs, bases = [], []
     for q, (handle, off) in enumerate(every):
         if q == rank:

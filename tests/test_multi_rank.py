@@ -146,6 +146,38 @@ def _exchange_worker(rank, world, port, result_dir):
         dist.destroy_process_group()
 
 
+class _FailingAbi(_FakeAbi):
+    def scoup_ipc_export(self, dptr):
+        if self.rank == 1:
+            raise RuntimeError("no IPC here")
+        return super().scoup_ipc_export(dptr)
+
+
+def _exchange_fail_worker(rank, world, port, result_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            D.exchange_accumulators(_FakeW(1), rank, world, device=0, abi_mod=_FailingAbi(rank))
+            msg = "no error"
+        except RuntimeError as ex:
+            msg = "raised" if "export" in str(ex) or "IPC" in str(ex) else str(ex)
+        with open(os.path.join(result_dir, f"fx{rank}.txt"), "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_accumulator_exchange_failure_is_collective(tmp_path):
+    """If one rank cannot export its accumulator, every rank raises (none is left waiting in a
+    collective), so the caller can fall back to the NCCL reduce-scatter on all ranks."""
+    mp.spawn(_exchange_fail_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        assert open(os.path.join(tmp_path, f"fx{r}.txt")).read() == "raised"
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_accumulator_exchange_over_gloo(tmp_path, world):
     """The host side of the fused cross-rank reduction (distributed.exchange_accumulators): every
