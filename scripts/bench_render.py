@@ -87,6 +87,8 @@ def main():
     # decode is an fp32 GEMM [HW, L] x [L, D]: flops and its operand/result bytes per view
     flops = 2.0 * H * W * L * args.D
     byts = 4.0 * (H * W * L + L * args.D + H * W * args.D)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    dec_gbs = byts / (res["decode"] * 1e-3) / 1e9
     print(json.dumps({
         "metric": "Eq. 7 sparse coefficient render + Eq. 8 decode, ms per view",
         "config": {"workload": f"{args.config}: {g.count} Gaussians, {cfg.num_views} views {W}x{H}, L={L}, "
@@ -96,6 +98,9 @@ def main():
         "decode_gbps": byts / (res["decode"] * 1e-3) / 1e9,
         "fill_gbps": 4.0 * H * W * args.D / (res["fill"] * 1e-3) / 1e9,
         "render_out_gbps": 4.0 * H * W * L / (res["render"] * 1e-3) / 1e9,
+        "decode_roofline": {"bound": "hbm", "kernel": "decode_kernel (tcgen05 3xTF32)", "achieved": dec_gbs,
+                            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": dec_gbs / peaks["hbm_gbs"],
+                            "bytes": "4 L read + 4 D written per pixel (+ the codebook)"},
         "dtype": "f32", "data": "synthetic",
     }))
 
