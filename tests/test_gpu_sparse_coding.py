@@ -192,3 +192,55 @@ def test_sparse_coding_errors(dev):
     with pytest.raises(abi.ScoupError) as ei:
         SparseCoder(torch.zeros((10, 1024), device="cuda"), 128, 4)
     assert ei.value.status == 6
+
+
+def test_pipeline_sparse_codes_into_uplift(dev, tiny_scene):
+    """Eq. 4 -> Eq. 5/6: region features of the tiny scene (one CLIP-like vector per (view,
+    region), R = 4 x 16) are sparse-coded on the GPU (k-means + 300 epochs, L = 64, K = 4); the
+    hard codes are the code table of the uplift (S = K), whose W / Z / codes equal the oracle's
+    uplift of the same codes."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    import oracle
+    sys_path_helpers()
+    from helpers import compare_codes
+    cfg, scene, maps, _ = tiny_scene
+    R = int(sum(synth.make_codes(cfg, seed=0).num_regions))
+    rf = synth.make_region_features(R, 128, 24, 4, noise=0.05, seed=21)
+    u, E = synth.make_kmeans_draws(cfg.L, 128, seed=21)
+    coder = _coder(rf.F, cfg.L, 4)
+    try:
+        coder.kmeans(u, E)
+        coder.train(300)
+        atoms, coefs = coder.encode()
+        atoms_np = atoms.cpu().numpy().view(np.uint32)
+        coefs_np = coefs.cpu().numpy()
+    finally:
+        coder.close()
+    assert np.allclose(coefs_np.sum(axis=1), 1.0, atol=1e-6) and (coefs_np > 0).all()
+    base = synth.make_codes(cfg, seed=0)
+    codes = synth.Codes(atoms_np, coefs_np, base.row0, base.num_regions)
+    Wo, Zo, fo, ao, co = oracle.uplift(scene.gaussians, scene.cameras, maps, codes, cfg.L, 4)
+    g = scene.gaussians
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    up = SparseUplift(gin, cfg.L, 4)
+    try:
+        up.add_views(scene.cameras, torch.from_numpy(np.ascontiguousarray(maps).view(np.int32)).cuda(),
+                     synth.Codes(atoms, coefs, base.row0, base.num_regions))
+        a2, c2 = up.finalize()
+        W = up.W[:g.count].double().cpu().numpy()
+        Z = up.Z[:g.count].double().cpu().numpy()
+    finally:
+        up.close()
+    assert np.all(np.abs(W - Wo) <= 1e-6 + 1e-4 * np.abs(Wo))
+    assert np.all(np.abs(Z - Zo) <= 1e-6 + 1e-4 * np.abs(Zo))
+    bad, _, worst = compare_codes(a2.cpu().numpy().view(np.uint32), c2.cpu().numpy(), Wo, 4)
+    assert bad == 0, worst
+
+
+def sys_path_helpers():
+    import os
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    if here not in sys.path:
+        sys.path.insert(0, here)
