@@ -248,10 +248,9 @@ def main():
         except Exception as ex:  # noqa: BLE001 -- reported, then the NCCL path
             print(f"[rank {rank}] fused exchange unavailable ({ex}); using NCCL reduce-scatter", file=sys.stderr)
             exchange = "nccl"
-        flags = [exchange == "fused"] * 1
-        allf = [None] * world
-        dist.all_gather_object(allf, flags[0])
-        if not all(allf):
+        everyone = [None] * world  # the fused path only if every rank has its mappings
+        dist.all_gather_object(everyone, exchange == "fused")
+        if not all(everyone):
             exchange = "nccl"
 
     def finalize_all(u, out_atoms=None, out_coefs=None):
