@@ -48,8 +48,13 @@ def main():
     codes = synth.Codes(torch.from_numpy(ch.atoms.view(np.int32)).to(dev), torch.from_numpy(ch.coefs).to(dev),
                         ch.row0, ch.num_regions)
     up = SparseUplift(gd, cfg.L, cfg.K)
+    up.set_counters(True)  # the render evaluates exactly the uplift's fragments: count them once
     up.add_views(scene.cameras, maps, codes)
     atoms, coefs = up.finalize()
+    st = up.stats()
+    up.set_counters(False)
+    tests_v = st["support_tests"] / cfg.num_views
+    contrib_v = st["contributions"] / cfg.num_views
     del maps
     torch.cuda.synchronize()
     H, W, L, B = scene.cameras[0].height, scene.cameras[0].width, cfg.L, args.batch
@@ -89,6 +94,10 @@ def main():
     byts = 4.0 * (H * W * L + L * args.D + H * W * args.D)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     dec_gbs = byts / (res["decode"] * 1e-3) / 1e9
+    # render (Eq. 7): the uplift's 27 lane-ops per support test plus 2 K per contribution (K
+    # products coef * e and K adds into the pixel's row), against the FP32-lane peak
+    peak_lane = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    ren_ops = (27 * tests_v + 2 * cfg.K * contrib_v) / (res["render"] * 1e-3) / 1e12
     print(json.dumps({
         "metric": "Eq. 7 sparse coefficient render + Eq. 8 decode, ms per view",
         "config": {"workload": f"{args.config}: {g.count} Gaussians, {cfg.num_views} views {W}x{H}, L={L}, "
@@ -98,6 +107,9 @@ def main():
         "decode_gbps": byts / (res["decode"] * 1e-3) / 1e9,
         "fill_gbps": 4.0 * H * W * args.D / (res["fill"] * 1e-3) / 1e9,
         "render_out_gbps": 4.0 * H * W * L / (res["render"] * 1e-3) / 1e9,
+        "render_roofline": {"bound": "alu", "kernel": "render_kernel", "achieved": ren_ops, "peak": peak_lane,
+                            "unit": "T lane-ops/s", "frac": ren_ops / peak_lane,
+                            "support_tests_per_view": tests_v, "contributions_per_view": contrib_v},
         "decode_roofline": {"bound": "hbm", "kernel": "decode_kernel (tcgen05 3xTF32)", "achieved": dec_gbs,
                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": dec_gbs / peaks["hbm_gbs"],
                             "bytes": "4 L read + 4 D written per pixel (+ the codebook)"},
