@@ -221,8 +221,19 @@ __global__ void sc_codebook_kernel(ScDev p, int nblk) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const long long step = *p.step + 1;
     if (i < LD) {
-        float g = 0.f;
-        for (int c = 0; c < nblk; c++) g += p.partials[(int64_t)c * LD + i];
+        // the CTA partials in a fixed order: four interleaved running sums keep many loads in
+        // flight (the epoch stays deterministic)
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+        int c = 0;
+#pragma unroll 2
+        for (; c + 4 <= nblk; c += 4) {
+            g0 += __ldg(p.partials + (int64_t)c * LD + i);
+            g1 += __ldg(p.partials + (int64_t)(c + 1) * LD + i);
+            g2 += __ldg(p.partials + (int64_t)(c + 2) * LD + i);
+            g3 += __ldg(p.partials + (int64_t)(c + 3) * LD + i);
+        }
+        for (; c < nblk; c++) g0 += __ldg(p.partials + (int64_t)c * LD + i);
+        const float g = (g0 + g1) + (g2 + g3);
         const float bc1 = (float)(1.0 - pow((double)p.b1, (double)step));
         const float bc2 = (float)(1.0 - pow((double)p.b2, (double)step));
         const float m = p.b1 * p.mC[i] + (1.0f - p.b1) * g;
