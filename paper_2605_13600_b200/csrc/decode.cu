@@ -11,9 +11,9 @@
 // in fp32 in tensor memory: the dropped A_small B_small term and the tf32 reading of `small` are
 // both below 2^-20 relative per product, i.e. the result matches an fp32 GEMM to ~1e-6.
 //
-// One persistent CTA per SM (8 warps, warp-specialised), a fixed N tile of NT = 256 columns of F
+// One persistent CTA per SM (12 warps, warp-specialised), a fixed N tile of NT = 256 columns of F
 // (B = C^T[NT, L] split big/small, resident in shared memory), looping over 128-row M tiles:
-//   * 4 producer warps: each A tile (128 x L fp32) is split and written to shared memory in the
+//   * 8 producer warps: each A tile (128 x L fp32) is split and written to shared memory in the
 //     K-major no-swizzle canonical UMMA layout (core matrices of 8 rows x 16 B; LBO = 128 B,
 //     SBO = chunks-per-row * 128 B, which makes the layout linear in the 16-byte chunk index, so
 //     the stores are contiguous).  The tile is handled in K parts with their own smem regions
@@ -37,7 +37,10 @@ namespace scoup {
 namespace {
 
 constexpr int DM = 128;           // rows per M tile (UMMA M)
-constexpr int NUM_PROD = 4;                    // producer warps (A split + MMA issue)
+#ifndef DEC_NPROD
+#define DEC_NPROD 8
+#endif
+constexpr int NUM_PROD = DEC_NPROD;            // producer warps (A split + MMA issue)
 constexpr int NUM_EPI = 4;                     // epilogue warps (1 per TMEM lane quarter)
 #ifndef DEC_NB
 #define DEC_NB 2
