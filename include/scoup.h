@@ -220,6 +220,17 @@ scoup_status scoup_uplift_finalize_topk_level(scoup_uplift *h, int32_t level, in
                                               float *out_coefs);
 
 /*
+ * finalize_topk_level plus, per row, the entropy of the Gaussian's aggregated coefficient
+ * distribution before Top-K: with
+ * w_l = W_l / sum_l W_l (Z cancels; negative-free by construction),
+ * H = -sum_l w_l ln w_l, computed in the same pass over the row (fp32; NaN for W_i == 0).
+ * out_entropy: device float [num_rows] (NULL = none).  Otherwise as finalize_topk_level.
+ */
+scoup_status scoup_uplift_finalize_topk_entropy(scoup_uplift *h, int32_t level, int64_t first_row, int64_t num_rows,
+                                                const float *W_rows, const float *Z_rows, uint32_t *out_atoms,
+                                                float *out_coefs, float *out_entropy);
+
+/*
  * Fused cross-rank reduction + Top-K (Eq. 5 is a sum over views, so
  * the ranks' view-sharded partials add; Eq. 6, on the sum).  Rows [first_row,
  * first_row + num_rows) of level `level`: W = sum over q < num_peers of W_peers[q] (summed in

@@ -188,3 +188,17 @@ def uplift(g, cams, region_maps, codes, L: int, K: int):
                                     codes.num_regions, L, K)
     atoms, coefs = topk(W, K)
     return W, Z, frags, atoms, coefs
+
+
+def entropy(W: np.ndarray) -> np.ndarray:
+    """H(w_i) = -sum_l w_il ln w_il of the aggregated coefficient
+    distribution before Top-K, w_i = W_i / sum_l W_il (Z cancels); 0 ln 0 = 0; NaN for W_i = 0.
+    Plain float64 numpy."""
+    W = np.asarray(W, dtype=np.float64)
+    S = W.sum(axis=1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        w = W / S[:, None]
+        terms = np.where(w > 0, w * np.log(np.where(w > 0, w, 1.0)), 0.0)
+        H = -terms.sum(axis=1)
+    H[~(S > 0)] = np.nan
+    return H

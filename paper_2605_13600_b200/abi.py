@@ -45,7 +45,7 @@ class scoup_timing(C.Structure):
 
 EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
            "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
-           "scoup_uplift_render_views", "scoup_uplift_decode", "scoup_uplift_finalize_topk_peers",
+           "scoup_uplift_render_views", "scoup_uplift_decode", "scoup_uplift_finalize_topk_peers", "scoup_uplift_finalize_topk_entropy",
            "scoup_ipc_export", "scoup_ipc_import", "scoup_ipc_close",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
@@ -83,6 +83,7 @@ def lib():
         L.scoup_uplift_free.restype = None
         L.scoup_last_error.restype = C.c_char_p
         L.scoup_uplift_finalize_topk_peers.argtypes = [P, i32, i64, i64, i32, P, P, P]
+        L.scoup_uplift_finalize_topk_entropy.argtypes = [P, i32, i64, i64, P, P, P, P, P]
         L.scoup_ipc_export.argtypes = [P, P, C.POINTER(i64)]
         L.scoup_ipc_import.argtypes = [C.c_int, P, i64, C.POINTER(P), C.POINTER(P)]
         L.scoup_ipc_close.argtypes = [C.c_int, P]
@@ -318,3 +319,9 @@ def scoup_ipc_import(device: int, handle: bytes, offset: int):
 
 def scoup_ipc_close(device: int, base: int) -> None:
     _check(lib().scoup_ipc_close(device, base))
+
+
+def scoup_uplift_finalize_topk_entropy(h: int, level: int, first_row: int, num_rows: int, W_rows, Z_rows, out_atoms,
+                                       out_coefs, out_entropy) -> None:
+    _check(lib().scoup_uplift_finalize_topk_entropy(h, level, first_row, num_rows, ptr(W_rows), ptr(Z_rows),
+                                                    ptr(out_atoms), ptr(out_coefs), ptr(out_entropy)))

@@ -1060,6 +1060,13 @@ scoup_status scoup_uplift_finalize_topk(scoup_uplift* h, int64_t first_row, int6
 scoup_status scoup_uplift_finalize_topk_level(scoup_uplift* h, int32_t level, int64_t first_row, int64_t num_rows,
                                               const float* W_rows, const float* Z_rows, uint32_t* out_atoms,
                                               float* out_coefs) {
+    return scoup_uplift_finalize_topk_entropy(h, level, first_row, num_rows, W_rows, Z_rows, out_atoms, out_coefs,
+                                              nullptr);
+}
+
+scoup_status scoup_uplift_finalize_topk_entropy(scoup_uplift* h, int32_t level, int64_t first_row, int64_t num_rows,
+                                                const float* W_rows, const float* Z_rows, uint32_t* out_atoms,
+                                                float* out_coefs, float* out_entropy) {
     g_last_error.clear();
     (void)Z_rows;
     if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
@@ -1087,7 +1094,9 @@ scoup_status scoup_uplift_finalize_topk_level(scoup_uplift* h, int32_t level, in
                 }
                 CK(cudaEventRecord(h->topk_ev[0], h->stream));
             }
-            launch_topk(Wsrc, num_rows, valid, h->L, h->K, da, dc, h->stream);
+            if (out_entropy && !is_device_ptr(out_entropy))
+                return fail(SCOUP_EINVAL, "out_entropy must be device memory");
+            launch_topk(Wsrc, num_rows, valid, h->L, h->K, da, dc, out_entropy, h->stream);
             h->kernel_launches += 1;
             if (h->timing) {
                 CK(cudaEventRecord(h->topk_ev[1], h->stream));

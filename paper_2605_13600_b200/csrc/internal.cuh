@@ -386,7 +386,7 @@ struct RasterParams {
 void launch_raster(const RasterParams& p, cudaStream_t s);
 void launch_render(const RasterParams& p, cudaStream_t s);
 
-void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
-                 float* coefs, cudaStream_t s);
+void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms, float* coefs,
+                 float* entropy, cudaStream_t s);
 
 }  // namespace scoup

@@ -522,14 +522,19 @@ __global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const
 // current KMAX-th, so equal values keep the lower atom (atoms are scanned ascending).
 // Only positive values enter (registers start at 0).  Z_i cancels in the L1
 // renormalisation, so selection runs on the raw sums.
+// Optional by-product: the entropy of the
+// Gaussian's aggregated coefficient distribution before Top-K, w_l = W_l / sum W (Z cancels),
+// H = -sum_l w_l ln w_l = ln S - (sum_l W_l ln W_l) / S with S = sum_l W_l, accumulated in the
+// same pass (fp32; NaN for an empty row).
 template <int KMAX>
 __global__ void __launch_bounds__(128) topk_kernel(const float* __restrict__ W, int64_t rows, int64_t valid_rows,
                                                    int L, int K, uint32_t* __restrict__ atoms,
-                                                   float* __restrict__ coefs) {
+                                                   float* __restrict__ coefs, float* __restrict__ entropy) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     float bv[KMAX];
     uint32_t ba[KMAX];
+    float hs = 0.f, hw = 0.f;  // sum W, sum W ln W
 #pragma unroll
     for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
     if (r < valid_rows) {
@@ -537,6 +542,14 @@ __global__ void __launch_bounds__(128) topk_kernel(const float* __restrict__ W, 
         for (int c4 = 0; c4 < L / 4; c4++) {
             float4 v4 = __ldg(row + c4);
             float vals[4] = {v4.x, v4.y, v4.z, v4.w};
+            if (entropy) {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (vals[u] > 0.f) {
+                        hs += vals[u];
+                        hw += vals[u] * logf(vals[u]);
+                    }
+            }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 float v = vals[u];
@@ -568,22 +581,29 @@ __global__ void __launch_bounds__(128) topk_kernel(const float* __restrict__ W, 
             coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
         }
     }
+    if (entropy) entropy[r] = hs > 0.f ? fmaxf(0.f, logf(hs) - hw / hs) : __int_as_float(0x7fc00000);
 }
 
 // generic L (not a multiple of 4): scalar loads
 template <int KMAX>
 __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restrict__ W, int64_t rows,
                                                           int64_t valid_rows, int L, int K,
-                                                          uint32_t* __restrict__ atoms, float* __restrict__ coefs) {
+                                                          uint32_t* __restrict__ atoms, float* __restrict__ coefs,
+                                                          float* __restrict__ entropy) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     float bv[KMAX];
     uint32_t ba[KMAX];
+    float hs = 0.f, hw = 0.f;
 #pragma unroll
     for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
     if (r < valid_rows) {
         for (int c = 0; c < L; c++) {
             float v = __ldg(W + r * (int64_t)L + c);
+            if (entropy && v > 0.f) {
+                hs += v;
+                hw += v * logf(v);
+            }
             if (v > bv[KMAX - 1]) {
                 uint32_t a = (uint32_t)c;
 #pragma unroll
@@ -611,6 +631,7 @@ __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restric
             coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
         }
     }
+    if (entropy) entropy[r] = hs > 0.f ? fmaxf(0.f, logf(hs) - hw / hs) : __int_as_float(0x7fc00000);
 }
 
 }  // namespace
@@ -778,20 +799,21 @@ void launch_topk_peers(const PeerRows& peers, int64_t first_row, int64_t rows, i
 
 template <int KMAX>
 static void topk_dispatch(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
-                          float* coefs, cudaStream_t s) {
+                          float* coefs, float* entropy, cudaStream_t s) {
     if (L % 4 == 0 && (reinterpret_cast<uintptr_t>(W) % 16) == 0)
-        topk_kernel<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs);
+        topk_kernel<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs, entropy);
     else
-        topk_kernel_scalar<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs);
+        topk_kernel_scalar<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs,
+                                                                     entropy);
 }
 
 void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms, float* coefs,
-                 cudaStream_t s) {
+                 float* entropy, cudaStream_t s) {
     if (rows <= 0) return;
-    if (K <= 4) topk_dispatch<4>(W, rows, valid_rows, L, K, atoms, coefs, s);
-    else if (K <= 8) topk_dispatch<8>(W, rows, valid_rows, L, K, atoms, coefs, s);
-    else if (K <= 16) topk_dispatch<16>(W, rows, valid_rows, L, K, atoms, coefs, s);
-    else topk_dispatch<32>(W, rows, valid_rows, L, K, atoms, coefs, s);
+    if (K <= 4) topk_dispatch<4>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 8) topk_dispatch<8>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 16) topk_dispatch<16>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else topk_dispatch<32>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
 }
 
 }  // namespace scoup

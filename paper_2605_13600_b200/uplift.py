@@ -89,6 +89,16 @@ class SparseUplift:
                                              out_coefs)
         return out_atoms, out_coefs
 
+    def finalize_with_entropy(self, first_row: int = 0, num_rows=None, level: int = 0):
+        """Eq. 6 codes plus the pre-Top-K coefficient entropy H_i of each row."""
+        torch = _torch()
+        num_rows = self.G - first_row if num_rows is None else num_rows
+        atoms = torch.empty((num_rows, self.K), dtype=torch.int32, device=self.device)
+        coefs = torch.empty((num_rows, self.K), dtype=torch.float32, device=self.device)
+        H = torch.empty((num_rows,), dtype=torch.float32, device=self.device)
+        abi.scoup_uplift_finalize_topk_entropy(self._h, level, first_row, num_rows, None, None, atoms, coefs, H)
+        return atoms, coefs, H
+
     def render(self, cameras: Sequence, atoms, coefs, out=None):
         """Eq. 7: per-pixel sum of the stored K-sparse codes w_hat_i e_i(v,p) -> [V, H, W, L] float32."""
         torch = _torch()

@@ -617,3 +617,31 @@ def test_fused_peer_reduce_topk_matches_oracle(dev, tiny_scene, world):
     Cc = np.concatenate(coefs)[:g.count]
     bad, ties, worst = compare_codes(A, Cc, Wo, cfg.K)
     assert bad == 0, worst
+
+
+def test_finalize_entropy_matches_oracle(dev, tiny_scene, tiny_oracle):
+    """the pre-Top-K coefficient entropy, computed in the Top-K pass,
+    equals the oracle's from its fp64 W (fp32 sums and logf: 1e-5 relative + 1e-6 absolute);
+    uncoded Gaussians get NaN on both sides; the codes of this entry point equal finalize's."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    Wo = tiny_oracle[0]
+    g = scene.gaussians
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    up = SparseUplift(gin, cfg.L, cfg.K)
+    try:
+        up.add_views(scene.cameras, torch.from_numpy(np.ascontiguousarray(maps).view(np.int32)).cuda(),
+                     synth.Codes(torch.from_numpy(codes.atoms.view(np.int32)).cuda(),
+                                 torch.from_numpy(codes.coefs).cuda(), codes.row0, codes.num_regions))
+        a1, c1 = up.finalize()
+        a2, c2, H = up.finalize_with_entropy()
+        H = H.double().cpu().numpy()
+        assert torch.equal(a1, a2) and torch.equal(c1, c2)
+    finally:
+        up.close()
+    Ho = oracle.entropy(Wo)
+    assert np.array_equal(np.isnan(H), np.isnan(Ho))
+    ok = ~np.isnan(Ho)
+    assert ok.sum() > 100
+    assert np.all(np.abs(H[ok] - Ho[ok]) <= 1e-6 + 1e-5 * np.abs(Ho[ok]))

@@ -485,3 +485,19 @@ def test_dense_feature_path(tiny_scene):
         np.add.at(F, gid, prod.astype(np.float64))
     assert np.allclose(Wd, F, rtol=1e-9, atol=1e-12)
     assert np.allclose(Z, Zd)
+
+
+def test_entropy_closed_forms():
+    """P:445-448 entropy pins: uniform over L atoms -> ln L; one-hot -> 0; two atoms p, 1-p ->
+    -p ln p - (1-p) ln(1-p); scaling a row (Z) does not change it; an empty row -> NaN."""
+    W = np.zeros((5, 8))
+    W[0] = 3.0
+    W[1, 5] = 0.2
+    W[2, :2] = (0.3, 0.7)
+    W[3, :2] = (30.0, 70.0)
+    H = oracle.entropy(W)
+    assert abs(H[0] - np.log(8)) < 1e-15
+    assert H[1] == 0.0
+    assert abs(H[2] - (-0.3 * np.log(0.3) - 0.7 * np.log(0.7))) < 1e-15
+    assert abs(H[3] - H[2]) < 1e-15
+    assert np.isnan(H[4])
