@@ -317,6 +317,60 @@ size_t decode_tc_scratch_bytes(int L, int D);
 cudaError_t launch_decode_tc(const float* W_hat, int64_t P, int L, int D, const float* C, float* scratch, float* F,
                              int num_sms, cudaStream_t s);
 
+// ---- paired FP32 (sm_100 FADD2 / FMUL2 / FFMA2): two independent IEEE round-to-nearest
+// operations per instruction; a pair lives in a 64-bit register (lo = first element)
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 f2_pack(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_split(f2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_sub(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f2 f2_rsub(f2 a, float s) { return f2_sub(f2_pack(s, s), a); }  // s - a
+__device__ __forceinline__ f2 f2_fmac(f2 a, f2 b, float c) { return f2_fma(a, b, f2_pack(c, c)); }
+
+// exp2_spec (internal.cuh) on a pair: the same operations element-wise.
+__device__ __forceinline__ f2 exp2_spec2(f2 y) {
+    const float magic = 0x1.8p23f;  // 1.5 * 2^23
+    const f2 mg = f2_pack(magic, magic);
+    const f2 t = f2_add(y, mg);
+    const f2 kf = f2_sub(t, mg);
+    const f2 f = f2_sub(y, kf);
+    f2 p = f2_fmac(f2_pack(0x1.5bba14p-10f, 0x1.5bba14p-10f), f, 0x1.3cea88p-7f);
+    p = f2_fmac(p, f, 0x1.c6b752p-5f);
+    p = f2_fmac(p, f, 0x1.ebf9bcp-3f);
+    p = f2_fmac(p, f, 0x1.62e42ap-1f);
+    p = f2_fmac(p, f, 1.0f);
+    float p0, p1, t0, t1;
+    f2_split(p, p0, p1);
+    f2_split(t, t0, t1);
+    return f2_pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                   __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
+
 // ---- launchers (kernels.cu) ----
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);

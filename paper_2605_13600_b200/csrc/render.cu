@@ -26,8 +26,12 @@ constexpr int MAX_RK = 32;  // stored code length K
 constexpr int KG = 8;       // code slots updated per independent group
 
 struct RRing {
-    float4 q0[QCAP + BATCH];  // (mx, my, r, o)
-    float4 q1[QCAP + BATCH];  // (qa, qb, qc, ycut)
+    // pair-interleaved (mx, mx', my, my'), (r, r', o, o'), (qa, qa', qb, qb'), (qc, qc', ycut,
+    // ycut') of records 2i, 2i+1, as in the uplift kernel (paired-FP32 evaluation)
+    float4 p0[(QCAP + BATCH) / 2];
+    float4 p1[(QCAP + BATCH) / 2];
+    float4 p2[(QCAP + BATCH) / 2];
+    float4 p3[(QCAP + BATCH) / 2];
     float4 q2[QCAP + BATCH];  // (support-box half-extents x, y, Gaussian id, sy)
     float4 q3[QCAP + BATCH];  // band_relevant parameters
 };
@@ -112,8 +116,19 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
     const float WX1 = (float)(min(wx0 + 8, Wd) - 1) + 0.5f, WY1 = (float)(min(wy0 + 4, Hd) - 1) + 0.5f;
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
     const unsigned lanemask_lt = (1u << lane) - 1u;
-    float4* const q0 = sm.r.q0;
-    float4* const q1 = sm.r.q1;
+    float* const pf0 = reinterpret_cast<float*>(sm.r.p0);
+    float* const pf1 = reinterpret_cast<float*>(sm.r.p1);
+    float* const pf2 = reinterpret_cast<float*>(sm.r.p2);
+    float* const pf3 = reinterpret_cast<float*>(sm.r.p3);
+    auto put_pair_rec = [&](uint32_t pos, const float4& r0, const float4& r1) {
+        const uint32_t b = (pos >> 1) * 4 + (pos & 1);
+        pf0[b] = r0.x; pf0[b + 2] = r0.y; pf1[b] = r0.z; pf1[b + 2] = r0.w;
+        pf2[b] = r1.x; pf2[b + 2] = r1.y; pf3[b] = r1.z; pf3[b + 2] = r1.w;
+    };
+    auto get_rec0 = [&](uint32_t pos) {
+        const uint32_t b = (pos >> 1) * 4 + (pos & 1);
+        return make_float4(pf0[b], pf0[b + 2], pf1[b], pf1[b + 2]);
+    };
     float4* const q2 = sm.r.q2;
     float4* const q3 = sm.r.q3;
     __syncthreads();
@@ -146,9 +161,9 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
             }
             if (accp) {
                 const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (QCAP - 1);
-                q0[pos] = r0; q1[pos] = r1; q2[pos] = r2; q3[pos] = r3;
+                put_pair_rec(pos, r0, r1); q2[pos] = r2; q3[pos] = r3;
                 if (pos < (uint32_t)BATCH) {
-                    q0[pos + QCAP] = r0; q1[pos + QCAP] = r1; q2[pos + QCAP] = r2; q3[pos + QCAP] = r3;
+                    put_pair_rec(pos + QCAP, r0, r1); q2[pos + QCAP] = r2; q3[pos + QCAP] = r3;
                 }
             }
             q_count += tot;
@@ -216,12 +231,40 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
         if (!warp_done && (uint32_t)lane < n)
-            rel = band_relevant(q0[q_head + lane], q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
+            rel = band_relevant(get_rec0(q_head + lane), q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
         const unsigned mask = __ballot_sync(FULL, rel);
-        for (int j = 0; j < BATCH; j++) {
-            if (!((mask >> j) & 1u)) continue;  // warp-uniform
-            bool con;
-            const float e = pixel_fragment(q0[q_head + j], q1[q_head + j], px, py, true, T, con);
+        const ulonglong2* b0 = reinterpret_cast<const ulonglong2*>(sm.r.p0) + (q_head >> 1);
+        const ulonglong2* b1 = reinterpret_cast<const ulonglong2*>(sm.r.p1) + (q_head >> 1);
+        const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(sm.r.p2) + (q_head >> 1);
+        const ulonglong2* b3 = reinterpret_cast<const ulonglong2*>(sm.r.p3) + (q_head >> 1);
+        for (int j2 = 0; j2 < BATCH; j2 += 2) {
+            const unsigned pm = (mask >> j2) & 3u;
+            if (!pm) continue;  // warp-uniform
+            // the T-independent part of DESIGN.md §3 PX for records j2, j2+1 in paired FP32
+            const ulonglong2 A0 = b0[j2 >> 1], A1 = b1[j2 >> 1], A2 = b2[j2 >> 1], A3 = b3[j2 >> 1];
+            const f2 dx2 = f2_rsub(A0.x, px), dy2 = f2_rsub(A0.y, py);
+            const f2 q2v = f2_fma(dx2, f2_fma(A2.x, dx2, f2_mul(A2.y, dy2)), f2_mul(f2_mul(A3.x, dy2), dy2));
+            float op0, op1, dxs[2], dys[2], qs[2], rs[2], ys[2];
+            f2_split(f2_mul(A1.y, exp2_spec2(q2v)), op0, op1);
+            const float al2[2] = {fminf(K_ACLAMP, op0), fminf(K_ACLAMP, op1)};
+            float om[2];
+            f2_split(f2_rsub(f2_pack(al2[0], al2[1]), 1.0f), om[0], om[1]);
+            f2_split(dx2, dxs[0], dxs[1]);
+            f2_split(dy2, dys[0], dys[1]);
+            f2_split(q2v, qs[0], qs[1]);
+            f2_split(A1.x, rs[0], rs[1]);
+            f2_split(A3.y, ys[0], ys[1]);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+            if (!((pm >> h) & 1u)) continue;  // warp-uniform
+            const int j = j2 + h;
+            const bool sq = fabsf(dxs[h]) <= rs[h] && fabsf(dys[h]) <= rs[h];
+            const float al = al2[h];
+            const float Tn = __fmul_rn(T, om[h]);
+            const bool pass = sq && !(qs[h] > 0.f) && qs[h] >= ys[h] && al >= K_AMIN;
+            const bool con = pass && !(Tn < K_TMIN);
+            const float e = con ? __fmul_rn(al, T) : 0.f;
+            T = con ? Tn : (pass ? 0.f : T);
             if (con) {
                 for (int k0 = 0; k0 < rKp; k0 += KG) {
                     const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.code_a[j][k0]);
@@ -236,6 +279,7 @@ __global__ void __launch_bounds__(TILE_PIX, 1) render_kernel(const RasterParams 
 #pragma unroll
                     for (int k = 0; k < KG; k++) acc[a[k]] = __fmaf_rn(c[k], e, v[k]);
                 }
+            }
             }
         }
         q_head = (q_head + n) & (QCAP - 1);
