@@ -70,23 +70,25 @@ __device__ __forceinline__ void warp_topk(const float (&z)[LPL], int K, int lane
             zs[k] = -INFINITY;
             continue;
         }
+        // the round's largest untaken logit (5 float shuffles), then its lowest index: the first
+        // entry slot i whose ballot of (untaken and equal) is non-empty, lowest lane in it
         float bv = -INFINITY;
-        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < LPL; i++)
+            if (!((taken >> i) & 1u)) bv = fmaxf(bv, z[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bv = fmaxf(bv, __shfl_xor_sync(FULL, bv, o));
+        int bi = -1;
 #pragma unroll
         for (int i = 0; i < LPL; i++) {
-            const int l = lane + 32 * i;
-            if (!((taken >> i) & 1u) && (z[i] > bv || (z[i] == bv && l < bi))) {
-                bv = z[i];
-                bi = l;
-            }
+            const unsigned b = __ballot_sync(FULL, !((taken >> i) & 1u) && z[i] == bv);
+            if (bi < 0 && b) bi = (__ffs(b) - 1) + 32 * i;
         }
+        if (bi < 0) {  // (non-finite logits only: the first untaken entry, never out of range)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(FULL, bv, o);
-            const int oi = __shfl_xor_sync(FULL, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-                bv = ov;
-                bi = oi;
+            for (int i = LPL - 1; i >= 0; i--) {
+                const unsigned b = __ballot_sync(FULL, !((taken >> i) & 1u));
+                if (b) bi = (__ffs(b) - 1) + 32 * i;
             }
         }
         sel[k] = bi;
