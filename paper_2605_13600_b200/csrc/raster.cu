@@ -45,27 +45,36 @@ constexpr int NWARP = TILE_PIX / 32;
 // Sum e[i] over the lanes in the group (all lanes if !MASKED); lane l returns the sum for i = l.
 template <bool MASKED>
 __device__ __forceinline__ float transpose_reduce(const float (&e)[BATCH], bool mine, int lane) {
+    // (the adds of sums i and i+1 go pairwise through FADD2: the same two IEEE adds)
     float v[16];
     {
         const bool up = lane & 16;
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            float lo = e[i], hi = e[i + 16];
-            if (MASKED) { lo = mine ? lo : 0.f; hi = mine ? hi : 0.f; }
-            const float send = up ? lo : hi;
-            const float keep = up ? hi : lo;
-            v[i] = keep + __shfl_xor_sync(FULL, send, 16);
+        for (int i = 0; i < 16; i += 2) {
+            float lo0 = e[i], hi0 = e[i + 16], lo1 = e[i + 1], hi1 = e[i + 17];
+            if (MASKED) {
+                lo0 = mine ? lo0 : 0.f; hi0 = mine ? hi0 : 0.f;
+                lo1 = mine ? lo1 : 0.f; hi1 = mine ? hi1 : 0.f;
+            }
+            const float r0 = __shfl_xor_sync(FULL, up ? lo0 : hi0, 16);
+            const float r1 = __shfl_xor_sync(FULL, up ? lo1 : hi1, 16);
+            f2_split(f2_add(f2_pack(up ? hi0 : lo0, up ? hi1 : lo1), f2_pack(r0, r1)), v[i], v[i + 1]);
         }
     }
 #pragma unroll
-    for (int s = 8; s >= 1; s >>= 1) {
+    for (int s = 8; s >= 2; s >>= 1) {
         const bool up = lane & s;
 #pragma unroll
-        for (int i = 0; i < s; i++) {
-            const float send = up ? v[i] : v[i + s];
-            const float keep = up ? v[i + s] : v[i];
-            v[i] = keep + __shfl_xor_sync(FULL, send, s);
+        for (int i = 0; i < s; i += 2) {
+            const float r0 = __shfl_xor_sync(FULL, up ? v[i] : v[i + s], s);
+            const float r1 = __shfl_xor_sync(FULL, up ? v[i + 1] : v[i + s + 1], s);
+            f2_split(f2_add(f2_pack(up ? v[i + s] : v[i], up ? v[i + s + 1] : v[i + 1]), f2_pack(r0, r1)), v[i],
+                     v[i + 1]);
         }
+    }
+    {
+        const bool up = lane & 1;
+        v[0] = (up ? v[1] : v[0]) + __shfl_xor_sync(FULL, up ? v[0] : v[1], 1);
     }
     return v[0];
 }
