@@ -90,6 +90,16 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.t.join(timeout=2)
+            if not any(len(ln.split(",")) >= 8 for ln in self.lines):
+                # a region shorter than nvidia-smi's first sample: one sample at its end
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=20)
+                    self.lines.extend(ln.strip() for ln in out.stdout.splitlines())
+                except Exception:
+                    pass
 
     def summary(self):
         sm, mx, reasons = [], [], set()
