@@ -122,6 +122,7 @@ struct Ctx {
     bool far_any = false;
     CamBatch cams{};
     const uint32_t* ids_dev[MAX_VB][MAX_LEV] = {};
+    int64_t far_cand = 0;  // visible Gaussians beyond the near split (for the near-fraction feedback)
     // timing: ring of event sets, 7 marks per batch (see ev_accumulate)
     struct EvSet { cudaEvent_t e[7]; bool pending; int views; };
     std::vector<EvSet> evs;
@@ -162,8 +163,14 @@ struct scoup_uplift {
     bool topk_pending = false;
     int64_t kernel_launches = 0, cub_launches = 0;
     double bb[6] = {0, 0, 0, 0, 0, 0};  // box of the valid means (x0, y0, z0, x1, y1, z1)
-    double near_frac = 0.05;             // near chunk: this fraction of each view's visible Gaussians
-    int bin_shift = 6;                  // bins of 2^bin_shift px squares
+    // near chunk: this fraction of each view's visible Gaussians.  Adapted between batches unless
+    // fixed by SCOUP_NEAR_FRAC: when most Gaussians beyond the split still reach a live tile (a
+    // compact scene), the split prunes little and the fraction doubles (<= 0.5); when almost
+    // none do (a deep scene whose tiles saturate early), it halves back (>= 0.05).  Any split is
+    // exact (DESIGN.md §5 a3), so this only moves work between the two chunks.
+    double near_frac = 0.05;
+    bool near_frac_fixed = false;
+    int bin_shift = 0;                  // bins of 2^bin_shift px squares (0: by image width)
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
     cublasHandle_t blas = nullptr;      // decode GEMM (Eq. 8), created on first use
     // host region maps: the whole call's maps are copied up front on a copy stream, in chunks of
@@ -327,6 +334,9 @@ void ev_mark(Ctx& c, int k) {
 // Bins: squares of 2^bin_shift px (default 64x64, SCOUP_BIN_SHIFT) holding the depth-ordered
 // candidates of the 16x16 tiles inside them; each tile filters its bin's list (band_relevant).
 Binning choose_binning(int Wd, int Hd, int bin_shift) {
+    // default: 64 px bins for wide images, 32 px below 1280 px (measured: outdoor 1600 px, indoor
+    // 988 px and small 512 px configs); SCOUP_BIN_SHIFT fixes it
+    if (bin_shift <= 0) bin_shift = Wd >= 1280 ? 6 : 5;
     Binning b;
     b.tiles_x = (Wd + TILE - 1) / TILE;
     b.tiles_y = (Hd + TILE - 1) / TILE;
@@ -432,6 +442,7 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     const int shift = c.key_bits > HIST_BITS ? c.key_bits - HIST_BITS : 0;
     int64_t n0 = 0;
     c.far_any = false;
+    c.far_cand = 0;
     for (int v = 0; v < c.nv; v++) {
         const uint32_t* hv = c.h_hist + (int64_t)v * NHIST;
         uint64_t total = 0;
@@ -453,6 +464,7 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
         if (cum < total) c.far_any = true;
         c.h_thr[v] = thr;
         n0 += (int64_t)cum;
+        c.far_cand += (int64_t)(total - cum);
     }
     ViewBuffers& b = c.vb;
     CK(cudaMemcpyAsync(b.thr, c.h_thr, sizeof(uint32_t) * c.nv, cudaMemcpyHostToDevice, c.s));
@@ -587,6 +599,11 @@ scoup_status step_near_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
 
 void step_far_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     CK(cudaEventSynchronize(c.ev));
+    if (!h->near_frac_fixed && c.far_any && c.far_cand > 0) {
+        const double kept = (double)*c.h_nsel / (double)c.far_cand;
+        if (kept > 0.25) h->near_frac = std::min(0.5, h->near_frac * 2.0);
+        else if (kept < 0.05) h->near_frac = std::max(0.05, h->near_frac * 0.5);
+    }
     chunk_front(h, c, a, c.far_any ? (int64_t)*c.h_nsel : 0);
     ev_mark(c, 4);
     CK(cudaEventRecord(c.ev, c.s));
@@ -791,7 +808,10 @@ scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num
         dalloc(&h->pg.s2, G, hs);
         if (const char* nf = std::getenv("SCOUP_NEAR_FRAC")) {
             const double f = std::atof(nf);
-            if (f > 0.0) h->near_frac = f;
+            if (f > 0.0) {
+                h->near_frac = f;
+                h->near_frac_fixed = true;
+            }
         }
         if (const char* bs = std::getenv("SCOUP_BIN_SHIFT")) {
             const int v = std::atoi(bs);
