@@ -645,3 +645,54 @@ def test_finalize_entropy_matches_oracle(dev, tiny_scene, tiny_oracle):
     ok = ~np.isnan(Ho)
     assert ok.sum() > 100
     assert np.all(np.abs(H[ok] - Ho[ok]) <= 1e-6 + 1e-5 * np.abs(Ho[ok]))
+
+
+def test_peer_finalize_single_peer_equals_finalize(dev, tiny_scene):
+    """finalize_topk_peers with one peer (the handle's own W) reproduces finalize_topk bit for bit
+    (the same row sums, the same Top-K), also on a ragged sub-range of rows."""
+    from paper_2605_13600_b200 import abi
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, maps, codes = tiny_scene
+    g = scene.gaussians
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    up = SparseUplift(gin, cfg.L, cfg.K)
+    try:
+        up.add_views(scene.cameras, torch.from_numpy(np.ascontiguousarray(maps).view(np.int32)).cuda(),
+                     synth.Codes(torch.from_numpy(codes.atoms.view(np.int32)).cuda(),
+                                 torch.from_numpy(codes.coefs).cuda(), codes.row0, codes.num_regions))
+        a1, c1 = up.finalize(37, 1001)
+        a2 = torch.empty_like(a1)
+        c2 = torch.empty_like(c1)
+        abi.scoup_uplift_finalize_topk_peers(up._h, 0, 37, 1001, [up.W.data_ptr()], a2, c2)
+        assert torch.equal(a1, a2) and torch.equal(c1, c2)
+        with pytest.raises(abi.ScoupError) as ei:  # more than SCOUP's 16 peers
+            abi.scoup_uplift_finalize_topk_peers(up._h, 0, 0, 10, [up.W.data_ptr()] * 17, a2, c2)
+        assert ei.value.status == 1
+    finally:
+        up.close()
+
+
+@pytest.mark.parametrize("K", [1, 32])
+def test_render_code_lengths(dev, tiny_scene, K):
+    """Eq. 7 with stored codes of K = 1 and K = 32 slots (half of them empty), against the oracle's
+    fragment lists."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    cfg, scene, _, _ = tiny_scene
+    g = scene.gaussians
+    rng = np.random.default_rng(K)
+    atoms = rng.integers(0, cfg.L, size=(g.count, K)).astype(np.uint32)
+    if K > 1:
+        atoms[:, K // 2:] = NONE
+    coefs = rng.uniform(0.1, 1.0, size=(g.count, K)).astype(np.float32)
+    gin = synth.Gaussians(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                            for a in (g.means, g.scales, g.rotations, g.opacities)])
+    up = SparseUplift(gin, cfg.L, min(K, 8))
+    try:
+        Wh = up.render(scene.cameras[:2], torch.from_numpy(atoms.view(np.int32)).cuda(),
+                       torch.from_numpy(coefs).cuda()).double().cpu().numpy()
+    finally:
+        up.close()
+    ref = oracle_render(g, scene.cameras[:2], atoms, coefs, cfg.L)
+    assert np.abs(ref).max() > 0.05
+    assert np.all(np.abs(Wh - ref) <= 1e-6 + 1e-5 * np.abs(ref))
