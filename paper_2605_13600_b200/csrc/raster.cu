@@ -15,8 +15,11 @@
 //           log2-domain quadratic form, the q <= 0 guard, alpha = min(0.99, o exp2_spec(q)), the
 //           alpha >= 1/255 skip and the T(1-alpha) < 1e-4 stop -- giving the weights
 //           e_i(v,p) = alpha_i T of PAPER.md Eq. 2, bit-identical to the CPU oracle.
-//           Control flow is warp-uniform (one uniform branch per group of records); the
-//           per-lane decisions are predicates/selects.
+//           Control flow is warp-uniform (one uniform branch per group of RGROUP records); the
+//           per-lane decisions are predicates/selects.  The T-independent part (dx, dy, q,
+//           o exp2_spec(q)) of records 2i and 2i+1 is evaluated together in paired FP32
+//           (FADD2/FMUL2/FFMA2: two independent IEEE round-to-nearest ops per instruction, so
+//           each half is bit-identical to the scalar spec); only the T chain runs per record.
 //
 // Aggregation (Eq. 5; Algorithm 1 lines 8-10), for all nlev semantic
 // levels of the pass at once (the levels share every fragment, only
