@@ -416,7 +416,12 @@ def main():
                          "traffic": traffic_view, "traffic_unit": "DRAM bytes per view (ncu)",
                          "traffic_source": traffic_src, "avg_launch_ms": ras_avg_s * 1e3,
                          "views_per_launch": tm["views_timed"] / launches,
+                         # raster event time over the summed event time of all stages (the stages of
+                         # the two view-batch contexts overlap), and the raster launches'
+                         # summed event time per step over the step time (> 1 when the two contexts'
+                         # raster launches overlap)
                          "share_of_step": tm["raster_ms"] / max(1e-9, total_dev_ms),
+                         "raster_time_over_step": ras_step_s * 1e3 / max(1e-9, ms_per_step),
                          "peak_source": f"{sms} SMs x 128 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
             "gpu_launches": int((st["kernel_launches"] + st["cub_launches"]) / max(1, args.steps)),
             "clocks": clocks,
