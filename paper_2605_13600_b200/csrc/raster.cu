@@ -284,6 +284,10 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int LS = nlev * S;  // W updates per (slot, Gaussian): every level's code
     const int ls_log2 = (LS & (LS - 1)) == 0 ? __ffs(LS) - 1 : -1;
     const int s_log2 = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
+    // ceil(2^32 / d) for the flush's divisions by d = LS, S when they are not powers of two:
+    // __umulhi(i, m) == i / d exactly when i * d < 2^32, i.e. for every flush index
+    // i < MAX_SLOTS * BATCH * LS while LS <= 2048 (larger LS: dense features at nlev * L > 2048)
+    const uint32_t ls_magic = 0xFFFFFFFFu / (uint32_t)LS + 1u, s_magic = 0xFFFFFFFFu / (uint32_t)S + 1u;
     for (int i = t; i < (p.dense ? 0 : nslot * LS); i += TILE_PIX) {  // (dense: read in the flush)
         const int q = i / LS, ls = i - q * LS, l = ls / S, s = ls - l * S;
         const uint32_t k = sm.slot_key[q][l];
@@ -509,14 +513,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                     ls = i & (LS - 1);
                     j = (i >> ls_log2) & (BATCH - 1);
                     q = i >> (ls_log2 + 5);
-                } else {
-                    q = i / (BATCH * LS);
-                    const int rem = i - q * (BATCH * LS);
-                    j = rem / LS;
-                    ls = rem - j * LS;
+                } else {  // (u = i / LS; BATCH is a power of two)
+                    const uint32_t u = LS <= 2048 ? __umulhi((uint32_t)i, ls_magic) : (uint32_t)i / (uint32_t)LS;
+                    ls = i - (int)u * LS;
+                    j = (int)(u & (BATCH - 1));
+                    q = (int)(u >> 5);
                 }
                 const float v = sm.acc[buf][q * BATCH + j];
-                const int l = s_log2 >= 0 ? ls >> s_log2 : ls / S;
+                const int l = s_log2 >= 0 ? ls >> s_log2 : (int)__umulhi((uint32_t)ls, s_magic);
                 uint32_t a;
                 float c;
                 if (p.dense) {  // dense features (Eq. 3 baseline): slot s is atom s, from the table

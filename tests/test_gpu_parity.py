@@ -335,6 +335,18 @@ def test_fused_levels_tiny(dev):
     assert_levels_parity(res, oras, cfg.K)
 
 
+def test_fused_levels_odd_code_length(dev):
+    """Two fused levels with S = 3 codes (nlev * S = 6 and S not powers of two: the flush's
+    index arithmetic by multiply-high instead of shifts) equal two separate oracle uplifts."""
+    cfg = synth.CONFIGS["tiny"].with_(regions=(8, 64), S=3, K=3, unassigned_frac=0.1)
+    scene = synth.make_scene(cfg, 11)
+    maps = [synth.make_region_maps_numpy(cfg, level=l, seed=11) for l in range(2)]
+    codes = [synth.make_codes(cfg, level=l, seed=11) for l in range(2)]
+    oras = [oracle.uplift(scene.gaussians, scene.cameras, maps[l], codes[l], cfg.L, cfg.K) for l in range(2)]
+    res = run_gpu_levels(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K)
+    assert_levels_parity(res, oras, cfg.K)
+
+
 def test_fused_levels_indoor_full_size(dev):
     """configs[2] at full size (1M Gaussians: 100 clusters + 10% shell, 988x731, Dirichlet(0.5)
     codes), its three nested levels (32 / 128 / 512 regions) fused in one pass, on 2 sampled
@@ -411,7 +423,7 @@ def run_gpu_dense(g, cams, maps, feats, D):
         up.close()
 
 
-@pytest.mark.parametrize("D", [64, 512])
+@pytest.mark.parametrize("D", [48, 64, 512])
 def test_dense_feature_uplift(dev, tiny_scene, D):
     """the dense feature uplift of Eq. 3 that SCOUP's sparse
     uplift replaces -- every region carries a full D-vector of CLIP-like features (both signs),
