@@ -285,8 +285,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     const int ls_log2 = (LS & (LS - 1)) == 0 ? __ffs(LS) - 1 : -1;
     const int s_log2 = (S & (S - 1)) == 0 ? __ffs(S) - 1 : -1;
     // ceil(2^32 / d) for the flush's divisions by d = LS, S when they are not powers of two:
-    // __umulhi(i, m) == i / d exactly when i * d < 2^32, i.e. for every flush index
-    // i < MAX_SLOTS * BATCH * LS while LS <= 2048 (larger LS: dense features at nlev * L > 2048)
+    // __umulhi(i, m) == i / d exactly when i * d < 2^32
     const uint32_t ls_magic = 0xFFFFFFFFu / (uint32_t)LS + 1u, s_magic = 0xFFFFFFFFu / (uint32_t)S + 1u;
     for (int i = t; i < (p.dense ? 0 : nslot * LS); i += TILE_PIX) {  // (dense: read in the flush)
         const int q = i / LS, ls = i - q * LS, l = ls / S, s = ls - l * S;
@@ -506,20 +505,8 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const int alive = __syncthreads_count(T > 0.f);
         if (!overflow) {
             // ---- flush: nlev*S reds per (slot, Gaussian) into W_level, one per Gaussian into Z
-            const int nitems = nslot * BATCH * LS;
-            for (int i = t; i < nitems; i += TILE_PIX) {
-                int q, j, ls;
-                if (ls_log2 >= 0) {  // nlev * S a power of two (every single-level BASELINE config)
-                    ls = i & (LS - 1);
-                    j = (i >> ls_log2) & (BATCH - 1);
-                    q = i >> (ls_log2 + 5);
-                } else {  // (u = i / LS; BATCH is a power of two)
-                    const uint32_t u = LS <= 2048 ? __umulhi((uint32_t)i, ls_magic) : (uint32_t)i / (uint32_t)LS;
-                    ls = i - (int)u * LS;
-                    j = (int)(u & (BATCH - 1));
-                    q = (int)(u >> 5);
-                }
-                const float v = sm.acc[buf][q * BATCH + j];
+            // one red of W update ls (level l = ls / S, code slot ls % S) of (slot q, record j)
+            auto red_one = [&](int q, int j, int ls, float v) {
                 const int l = s_log2 >= 0 ? ls >> s_log2 : (int)__umulhi((uint32_t)ls, s_magic);
                 uint32_t a;
                 float c;
@@ -536,6 +523,23 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 if (v > 0.f && a != NONE)
                     atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
                               __fmul_rn(c, v));
+            };
+            if (ls_log2 >= 0) {
+                // nlev * S a power of two (every single-level BASELINE config): the CTA's threads
+                // sweep all (slot, record, update) items, LS consecutive threads per sum
+                const int nitems = nslot * BATCH * LS;
+                for (int i = t; i < nitems; i += TILE_PIX)
+                    red_one(i >> (ls_log2 + 5), (i >> ls_log2) & (BATCH - 1), i & (LS - 1),
+                            sm.acc[buf][i >> ls_log2]);
+            } else {
+                // (u = i / LS by multiply-high, exact for i * LS < 2^32: every flush index while
+                // LS <= 2048; BATCH is a power of two.  A per-warp ballot over the (slot, record)
+                // sums that skips the zero ones was measured slower: indoor 106 -> 128 ms)
+                const int nitems = nslot * BATCH * LS;
+                for (int i = t; i < nitems; i += TILE_PIX) {
+                    const uint32_t u = LS <= 2048 ? __umulhi((uint32_t)i, ls_magic) : (uint32_t)i / (uint32_t)LS;
+                    red_one((int)(u >> 5), (int)(u & (BATCH - 1)), i - (int)u * LS, sm.acc[buf][u]);
+                }
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
