@@ -81,6 +81,12 @@ typedef struct {
     int64_t lane_evaluations; /* lanes that ran the per-pixel sequence on a record (32 per
                                  (warp, record) evaluated; counted with the support tests):
                                  support_tests / lane_evaluations is the raster's lane use */
+    int64_t batches[2];     /* view batches run by each of the two pipeline contexts */
+    int64_t near_frac_changes; /* in-call adaptations of the near-chunk fraction (DESIGN.md §5 a3) */
+    int64_t host_map_chunks;/* up-front host->device region-map copy chunks (host region_ids) */
+    double near_frac;       /* the near-chunk fraction now in use */
+    int64_t global_reds;    /* red.global.add.f32 issued by the fused kernel's flush into W and Z
+                               (lane level; counted with the support tests) */
 } scoup_stats;
 
 /* Per-kernel-class device time (CUDA events on the launching streams), accumulated while
@@ -275,6 +281,13 @@ scoup_status scoup_uplift_get_stats(scoup_uplift *h, scoup_stats *out);
  * tests (scoup_stats); off by default (the production kernel keeps no counters).  A call to
  * add_views with a contributions_out array always uses the instrumented kernel. */
 scoup_status scoup_uplift_set_counters(scoup_uplift *h, int enable);
+
+/* Number of pipeline contexts add_views alternates between: 2 (the default)
+ * overlaps one view batch's front (depth pass, selection, sorts) with the other's raster; 1 runs
+ * every step of every batch in order on one stream, so that per-kernel event times are each
+ * kernel's own duration (bench.py's roofline timing pass).  Results are identical.  EINVAL
+ * outside {1, 2}. */
+scoup_status scoup_uplift_set_pipeline(scoup_uplift *h, int contexts);
 
 /* Enable (1) / disable (0) per-kernel-class event timing; enabling clears the totals. */
 scoup_status scoup_uplift_set_timing(scoup_uplift *h, int enable);

@@ -172,6 +172,42 @@ def uplift_accumulate(g, cams: Sequence, region_maps: np.ndarray, code_atoms: np
     return W, Z, frags
 
 
+def uplift_accumulate_parallel(g, cams: Sequence, region_maps: np.ndarray, code_atoms, code_coefs, code_row0,
+                               num_regions, L: int, K: int, workers: int = 0):
+    """The same Eq. 5 accumulation, with the views split into `workers` contiguous shards run on
+    host threads (the C oracle releases the GIL: ctypes), each into its own fp64 partial, merged
+    in shard order (a fixed order, SPEC.md S:324's concurrency model).  The oracle's arithmetic
+    is untouched: only the view loop is distributed.  Returns (W, Z, frags) like
+    uplift_accumulate (sums equal up to fp64 reassociation)."""
+    from concurrent.futures import ThreadPoolExecutor
+    V = len(cams)
+    workers = max(1, min(V, workers or len(os.sched_getaffinity(0))))
+    bounds = [(V * k // workers, V * (k + 1) // workers) for k in range(workers)]
+    row0 = np.asarray(code_row0, np.int64)
+    nreg = np.asarray(num_regions, np.int32)
+
+    def shard(b):
+        v0, v1 = b
+        return uplift_accumulate(g, list(cams[v0:v1]), region_maps[v0:v1], code_atoms, code_coefs,
+                                 row0[v0:v1], nreg[v0:v1], L, K)
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        parts = list(ex.map(shard, bounds))
+    W, Z, frags = parts[0]
+    for Wp, Zp, _ in parts[1:]:
+        W += Wp
+        Z += Zp
+    return W, Z, np.concatenate([p[2] for p in parts])
+
+
+def uplift_parallel(g, cams, region_maps, codes, L: int, K: int, workers: int = 0):
+    """uplift() with the view loop on host threads (uplift_accumulate_parallel)."""
+    W, Z, frags = uplift_accumulate_parallel(g, cams, region_maps, codes.atoms, codes.coefs, codes.row0,
+                                             codes.num_regions, L, K, workers)
+    atoms, coefs = topk(W, K)
+    return W, Z, frags, atoms, coefs
+
+
 def topk(W: np.ndarray, K: int) -> Tuple[np.ndarray, np.ndarray]:
     """Eq. 6 per row (value desc, atom asc; positive only; fp64 L1 renormalisation)."""
     W = np.ascontiguousarray(W, dtype=np.float64)

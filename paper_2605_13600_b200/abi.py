@@ -35,7 +35,9 @@ class scoup_camera(C.Structure):
 class scoup_stats(C.Structure):
     _fields_ = [("views", C.c_int64), ("contributions", C.c_int64), ("tile_entries", C.c_int64),
                 ("visible", C.c_int64), ("support_tests", C.c_int64), ("kernel_launches", C.c_int64),
-                ("cub_launches", C.c_int64), ("lane_evaluations", C.c_int64)]
+                ("cub_launches", C.c_int64), ("lane_evaluations", C.c_int64), ("batches", C.c_int64 * 2),
+                ("near_frac_changes", C.c_int64), ("host_map_chunks", C.c_int64), ("near_frac", C.c_double),
+                ("global_reds", C.c_int64)]
 
 
 class scoup_timing(C.Structure):
@@ -49,10 +51,12 @@ EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_vi
            "scoup_ipc_export", "scoup_ipc_import", "scoup_ipc_close",
            "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
            "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
-           "scoup_uplift_free", "scoup_last_error", "scoup_version",
+           "scoup_uplift_set_pipeline", "scoup_uplift_free", "scoup_last_error", "scoup_version",
            # include/scoup_sparse_coding.h
            "scoup_sc_init", "scoup_sc_kmeans", "scoup_sc_set_state", "scoup_sc_get_state", "scoup_sc_train",
-           "scoup_sc_encode", "scoup_sc_free"]
+           "scoup_sc_encode", "scoup_sc_free",
+           # include/scoup_diag.h (measurement helpers)
+           "scoup_diag_red_rate", "scoup_diag_last_error"]
 
 _lib = None
 
@@ -78,6 +82,7 @@ def lib():
         L.scoup_uplift_get_stats.argtypes = [P, C.POINTER(scoup_stats)]
         L.scoup_uplift_set_counters.argtypes = [P, C.c_int]
         L.scoup_uplift_set_timing.argtypes = [P, C.c_int]
+        L.scoup_uplift_set_pipeline.argtypes = [P, C.c_int]
         L.scoup_uplift_get_timing.argtypes = [P, C.POINTER(scoup_timing)]
         L.scoup_uplift_free.argtypes = [P]
         L.scoup_uplift_free.restype = None
@@ -96,11 +101,16 @@ def lib():
         L.scoup_sc_free.argtypes = [P]
         L.scoup_sc_free.restype = None
         L.scoup_version.restype = C.c_char_p
+        L.scoup_diag_red_rate.argtypes = [C.c_int, i64, C.c_int, C.c_int, i64, C.c_int, C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double)]
+        L.scoup_diag_red_rate.restype = C.c_int
+        L.scoup_diag_last_error.restype = C.c_char_p
         for name in ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
                      "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
                      "scoup_uplift_render_views", "scoup_uplift_decode",
                      "scoup_uplift_reset", "scoup_uplift_get_accumulators", "scoup_uplift_get_stats",
-                     "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing"]:
+                     "scoup_uplift_set_counters", "scoup_uplift_set_timing", "scoup_uplift_get_timing",
+                     "scoup_uplift_set_pipeline"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -218,11 +228,17 @@ def scoup_uplift_get_accumulators(h: int):
 def scoup_uplift_get_stats(h: int) -> dict:
     s = scoup_stats()
     _check(lib().scoup_uplift_get_stats(h, C.byref(s)))
-    return {k: getattr(s, k) for k, _ in scoup_stats._fields_}
+    out = {k: getattr(s, k) for k, _ in scoup_stats._fields_}
+    out["batches"] = list(out["batches"])
+    return out
 
 
 def scoup_uplift_set_counters(h: int, enable: bool) -> None:
     _check(lib().scoup_uplift_set_counters(h, 1 if enable else 0))
+
+
+def scoup_uplift_set_pipeline(h: int, contexts: int) -> None:
+    _check(lib().scoup_uplift_set_pipeline(h, int(contexts)))
 
 
 def scoup_uplift_set_timing(h: int, enable: bool) -> None:
@@ -325,3 +341,14 @@ def scoup_uplift_finalize_topk_entropy(h: int, level: int, first_row: int, num_r
                                        out_coefs, out_entropy) -> None:
     _check(lib().scoup_uplift_finalize_topk_entropy(h, level, first_row, num_rows, ptr(W_rows), ptr(Z_rows),
                                                     ptr(out_atoms), ptr(out_coefs), ptr(out_entropy)))
+
+
+def scoup_diag_red_rate(device: int, buffer_bytes: int, scattered: bool, vec4: bool, reds_per_launch: int,
+                        launches: int):
+    """include/scoup_diag.h: (float adds per second, ms per launch) of red.global.add.f32 / v4."""
+    rate, ms = C.c_double(), C.c_double()
+    st = lib().scoup_diag_red_rate(device, int(buffer_bytes), int(scattered), int(vec4), int(reds_per_launch),
+                                   int(launches), C.byref(rate), C.byref(ms))
+    if st != 0:
+        raise ScoupError(st, lib().scoup_diag_last_error().decode())
+    return rate.value, ms.value

@@ -10,7 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu", "decode.cu", "sparse_coding.cu"]
+SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu", "decode.cu", "sparse_coding.cu", "diag.cu"]
 HEADERS = ["internal.cuh"]
 LIB = os.path.join(HERE, "libscoup.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -19,17 +19,26 @@ NVCC_FLAGS = [
     "-O3", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo",
-    # parity-critical arithmetic uses explicit _rn intrinsics; also forbid contraction
-    "-fmad=false",
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
 ]
+# The translation units of the parity-critical path (every fragment decision is
+# bit-identical to the oracle's) use explicit _rn intrinsics AND forbid contraction; the others
+# (Eq. 7 render accumulation, Eq. 8 decode, Eq. 4 sparse coding: tolerance-based parity) keep
+# nvcc's default FMA contraction.  (render.cu's per-pixel fragment sequence is written with
+# explicit intrinsics, which contraction never touches.)
+SPEC_TUS = {"api.cu", "kernels.cu", "raster.cu"}
+
+
+def tu_flags(src: str):
+    return ["-fmad=false"] if src in SPEC_TUS else []
 
 
 def _inputs():
     paths = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     paths.append(os.path.join(ROOT, "include", "scoup.h"))
     paths.append(os.path.join(ROOT, "include", "scoup_sparse_coding.h"))
+    paths.append(os.path.join(ROOT, "include", "scoup_diag.h"))
     paths.append(os.path.abspath(__file__))
     return paths
 
@@ -52,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     with tempfile.TemporaryDirectory(prefix="scoup_build_") as td:
         def compile_one(src: str) -> str:
             obj = os.path.join(td, os.path.splitext(src)[0] + ".o")
-            cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *flags, *tu_flags(src), "-c", os.path.join(CSRC, src), "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)

@@ -144,7 +144,7 @@ struct scoup_uplift {
     PackedGaussians pg{};
     int* d_err_code = nullptr;
     long long* d_err_index = nullptr;
-    unsigned long long* d_stats = nullptr;  // views, contributions, (unused), visible, support tests, lane evaluations
+    unsigned long long* d_stats = nullptr;  // views, contributions, global reds, visible, support tests, lane evaluations
     Ctx ctx[2];
     uint32_t* code_atoms = nullptr;
     float* code_coefs = nullptr;
@@ -172,6 +172,10 @@ struct scoup_uplift {
     bool near_frac_fixed = false;
     int bin_shift = 0;                  // bins of 2^bin_shift px squares (0: by image width)
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
+    int nctx = 2;                       // pipeline contexts in use (set_pipeline)
+    int64_t batches[2] = {0, 0};        // view batches per context (stats)
+    int64_t near_frac_changes = 0;      // in-call adaptations of near_frac (stats)
+    int64_t host_map_chunks = 0;        // up-front region-map copy chunks (stats)
     cublasHandle_t blas = nullptr;      // decode GEMM (Eq. 8), created on first use
     // host region maps: the whole call's maps are copied up front on a copy stream, in chunks of
     // MAX_VB views with one event each, so the PCIe transfer runs ahead of the batches
@@ -568,6 +572,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.contrib_ctr = h->d_stats + 1;
     p.support_ctr = h->d_stats + 4;
     p.lane_eval_ctr = h->d_stats + 5;
+    p.red_ctr = h->d_stats + 2;
     p.err = latch_of(h);
     ev_mark(c, mark0);
     if (a.render) launch_render(p, c.s);
@@ -601,8 +606,10 @@ void step_far_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     CK(cudaEventSynchronize(c.ev));
     if (!h->near_frac_fixed && c.far_any && c.far_cand > 0) {
         const double kept = (double)*c.h_nsel / (double)c.far_cand;
+        const double before = h->near_frac;
         if (kept > 0.25) h->near_frac = std::min(0.5, h->near_frac * 2.0);
         else if (kept < 0.05) h->near_frac = std::max(0.05, h->near_frac * 0.5);
+        if (h->near_frac != before) h->near_frac_changes++;
     }
     chunk_front(h, c, a, c.far_any ? (int64_t)*c.h_nsel : 0);
     ev_mark(c, 4);
@@ -661,6 +668,7 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
                                        region_ids[l] + (int64_t)v0 * npx, sizeof(uint32_t) * npx * nv,
                                        cudaMemcpyHostToDevice, h->copy_s));
                 CK(cudaEventRecord(h->chunk_ev[j], h->copy_s));
+                h->host_map_chunks++;
             }
         }
         int next = 0;  // first view not yet assigned to a batch
@@ -692,11 +700,11 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
         for (int ci = 0; ci < 2; ci++) h->ctx[ci].step = ST_IDLE;
         for (bool busy = true; busy && st == SCOUP_OK;) {
             busy = false;
-            for (int ci = 0; ci < 2 && st == SCOUP_OK; ci++) {
+            for (int ci = 0; ci < h->nctx && st == SCOUP_OK; ci++) {
                 Ctx& c = h->ctx[ci];
                 switch (c.step) {
                     case ST_IDLE:
-                        if (next < num_views) { start_batch(c); busy = true; }
+                        if (next < num_views) { start_batch(c); h->batches[ci]++; busy = true; }
                         break;
                     case ST_NEAR_FRONT: step_near_front(h, c, args); busy = true; break;
                     case ST_NEAR_RASTER: st = step_near_raster(h, c, args); busy = true; break;
@@ -1096,6 +1104,9 @@ scoup_status scoup_uplift_finalize_topk_entropy(scoup_uplift* h, int32_t level, 
     if (!W_rows && first_row + num_rows > h->Npad) return fail(SCOUP_EINVAL, "row range beyond rows_padded");
     try {
         DeviceGuard dg(h->device);
+        // (checked before any allocation or event record below)
+        if (num_rows > 0 && out_entropy && !is_device_ptr(out_entropy))
+            return fail(SCOUP_EINVAL, "out_entropy must be device memory");
         if (num_rows > 0) {
             const float* Wsrc =
                 W_rows ? W_rows : h->W + ((int64_t)level * h->Npad + first_row) * (int64_t)h->L;
@@ -1114,8 +1125,6 @@ scoup_status scoup_uplift_finalize_topk_entropy(scoup_uplift* h, int32_t level, 
                 }
                 CK(cudaEventRecord(h->topk_ev[0], h->stream));
             }
-            if (out_entropy && !is_device_ptr(out_entropy))
-                return fail(SCOUP_EINVAL, "out_entropy must be device memory");
             launch_topk(Wsrc, num_rows, valid, h->L, h->K, da, dc, out_entropy, h->stream);
             h->kernel_launches += 1;
             if (h->timing) {
@@ -1236,6 +1245,9 @@ scoup_status scoup_uplift_reset(scoup_uplift* h) {
         h->host_entries = 0;
         h->kernel_launches = 0;
         h->cub_launches = 0;
+        h->batches[0] = h->batches[1] = 0;
+        h->near_frac_changes = 0;
+        h->host_map_chunks = 0;
     } catch (const CudaError& e) {
         return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
     }
@@ -1266,6 +1278,12 @@ scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
         out->kernel_launches = h->kernel_launches;
         out->cub_launches = h->cub_launches;
         out->lane_evaluations = (int64_t)s[5];
+        out->global_reds = (int64_t)s[2];
+        out->batches[0] = h->batches[0];
+        out->batches[1] = h->batches[1];
+        out->near_frac_changes = h->near_frac_changes;
+        out->host_map_chunks = h->host_map_chunks;
+        out->near_frac = h->near_frac;
         return check_latched(h);
     } catch (const CudaError& e) {
         return fail(SCOUP_ECUDA, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.err));
@@ -1276,6 +1294,14 @@ scoup_status scoup_uplift_set_counters(scoup_uplift* h, int enable) {
     g_last_error.clear();
     if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
     h->count_tests = enable != 0;
+    return SCOUP_OK;
+}
+
+scoup_status scoup_uplift_set_pipeline(scoup_uplift* h, int contexts) {
+    g_last_error.clear();
+    if (!h) return fail(SCOUP_EINVAL, "handle is NULL");
+    if (contexts != 1 && contexts != 2) return fail(SCOUP_EINVAL, "contexts must be 1 or 2");
+    h->nctx = contexts;
     return SCOUP_OK;
 }
 

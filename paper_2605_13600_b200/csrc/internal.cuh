@@ -435,6 +435,7 @@ struct RasterParams {
     unsigned long long* contrib_ctr;  // handle stats
     unsigned long long* support_ctr;  // handle stats: support tests
     unsigned long long* lane_eval_ctr;  // handle stats: lane evaluations (32 per warp-record)
+    unsigned long long* red_ctr;  // handle stats: global reductions issued (lane level, W and Z)
     ErrorLatch err;
 };
 void launch_raster(const RasterParams& p, cudaStream_t s);

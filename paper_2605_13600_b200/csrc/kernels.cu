@@ -526,21 +526,49 @@ __global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const
 // Gaussian's aggregated coefficient distribution before Top-K, w_l = W_l / sum W (Z cancels),
 // H = -sum_l w_l ln w_l = ln S - (sum_l W_l ln W_l) / S with S = sum_l W_l, accumulated in the
 // same pass (fp32; NaN for an empty row).
+// Rows are staged through shared memory: the CTA's 128 consecutive rows (128 L floats,
+// contiguous in W) are read with coalesced float4 loads -- summed over the P partials in rank
+// order 0..P-1 for the fused cross-rank path (peers.n > 1) -- into padded shared rows (stride
+// L + 4 floats: a warp's LDS.128 of one column hits 8 distinct 16-B bank groups per wavefront),
+// then each thread runs the register insertion network on its own row.
+constexpr int TOPK_ROWS = 128;
+
 template <int KMAX>
-__global__ void __launch_bounds__(128) topk_kernel(const float* __restrict__ W, int64_t rows, int64_t valid_rows,
-                                                   int L, int K, uint32_t* __restrict__ atoms,
-                                                   float* __restrict__ coefs, float* __restrict__ entropy) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, int64_t rows, int64_t valid_rows, int L,
+                                                              int K, uint32_t* __restrict__ atoms,
+                                                              float* __restrict__ coefs, float* __restrict__ entropy) {
+    extern __shared__ __align__(16) float tile[];
+    const int LP = L + 4, L4 = L >> 2;
+    const int R = blockDim.x;  // rows per tile (one per thread)
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int64_t left = valid_rows - r0;
+    const int nr = left < (int64_t)R ? (int)left : R;  // rows of this tile to read
+    const int t = threadIdx.x;
+    for (int i = t; i < nr * L4; i += R) {
+        const int rr = i / L4, c4 = i - rr * L4;
+        const int64_t g = r0 * L4 + i;  // float4 index in the (contiguous) row block
+        float4 v4 = __ldg(reinterpret_cast<const float4*>(peers.W[0]) + g);
+        for (int q = 1; q < peers.n; q++) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(peers.W[q]) + g);
+            v4.x = __fadd_rn(v4.x, w4.x);
+            v4.y = __fadd_rn(v4.y, w4.y);
+            v4.z = __fadd_rn(v4.z, w4.z);
+            v4.w = __fadd_rn(v4.w, w4.w);
+        }
+        *reinterpret_cast<float4*>(tile + rr * LP + 4 * c4) = v4;
+    }
+    __syncthreads();
+    const int64_t r = r0 + t;
     if (r >= rows) return;
     float bv[KMAX];
     uint32_t ba[KMAX];
     float hs = 0.f, hw = 0.f;  // sum W, sum W ln W
 #pragma unroll
     for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
-    if (r < valid_rows) {
-        const float4* row = reinterpret_cast<const float4*>(W + r * (int64_t)L);
-        for (int c4 = 0; c4 < L / 4; c4++) {
-            float4 v4 = __ldg(row + c4);
+    if (t < nr) {
+        const float4* row = reinterpret_cast<const float4*>(tile + t * LP);
+        for (int c4 = 0; c4 < L4; c4++) {
+            const float4 v4 = row[c4];
             float vals[4] = {v4.x, v4.y, v4.z, v4.w};
             if (entropy) {
 #pragma unroll
@@ -730,90 +758,57 @@ void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_
 // Fused cross-rank reduction + Top-K (SURVEY.md §8(e)'s fusion option): the rows of this rank's
 // shard are summed over the P ranks' partial accumulators in place -- read directly from the
 // peers' memory (CUDA IPC mappings over NVLink / NVSwitch), in rank order 0..P-1 -- and Eq. 6
-// runs on the sums in registers.  This replaces reduce-scatter + Top-K: no reduced shard is
-// written and re-read.  One thread per row; float4 loads of each peer's row.
+// runs on the sums (topk_tile_kernel with P partials).  This replaces reduce-scatter + Top-K: no
+// reduced shard is written and re-read.
 template <int KMAX>
-__global__ void __launch_bounds__(128) topk_peers_kernel(PeerRows peers, int64_t first_row, int64_t rows,
-                                                         int64_t valid_rows, int L, int K,
-                                                         uint32_t* __restrict__ atoms, float* __restrict__ coefs) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    float bv[KMAX];
-    uint32_t ba[KMAX];
-#pragma unroll
-    for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
-    if (r < valid_rows) {
-        const int64_t off = (first_row + r) * (int64_t)L;
-        for (int c4 = 0; c4 < L / 4; c4++) {
-            float4 v4 = __ldg(reinterpret_cast<const float4*>(peers.W[0] + off) + c4);
-            for (int q = 1; q < peers.n; q++) {
-                const float4 w4 = __ldg(reinterpret_cast<const float4*>(peers.W[q] + off) + c4);
-                v4.x = __fadd_rn(v4.x, w4.x);
-                v4.y = __fadd_rn(v4.y, w4.y);
-                v4.z = __fadd_rn(v4.z, w4.z);
-                v4.w = __fadd_rn(v4.w, w4.w);
-            }
-            float vals[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                float v = vals[u];
-                if (v > bv[KMAX - 1]) {
-                    uint32_t a = (uint32_t)(c4 * 4 + u);
-#pragma unroll
-                    for (int s = 0; s < KMAX; s++) {
-                        bool sw = v > bv[s];
-                        float tv = sw ? bv[s] : v;
-                        uint32_t ta = sw ? ba[s] : a;
-                        bv[s] = sw ? v : bv[s];
-                        ba[s] = sw ? a : ba[s];
-                        v = tv;
-                        a = ta;
-                    }
-                }
-            }
-        }
+static void topk_tile_launch(PeerRows peers, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                             float* coefs, float* entropy, cudaStream_t s) {
+    const int R = L <= 256 ? TOPK_ROWS : 32;  // rows per CTA: <= 133 KB of staged rows (L <= SCOUP_MAX_L)
+    const size_t smem = (size_t)R * (L + 4) * sizeof(float);
+    static int smem_set = 0;  // opt-in above 48 KB, once per instantiation and size
+    if (smem > 48 * 1024 && smem_set < (int)smem) {
+        cudaFuncSetAttribute(topk_tile_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set = (int)smem;
     }
-    float sum = 0.f;
-#pragma unroll
-    for (int s = 0; s < KMAX; s++)
-        if (s < K) sum = __fadd_rn(sum, bv[s]);
-#pragma unroll
-    for (int s = 0; s < KMAX; s++) {
-        if (s < K) {
-            bool keep = bv[s] > 0.f;
-            atoms[r * K + s] = keep ? ba[s] : NONE;
-            coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
-        }
-    }
+    topk_tile_kernel<KMAX><<<grid_for(rows, R), R, smem, s>>>(peers, rows, valid_rows, L, K, atoms, coefs, entropy);
+}
+
+static void topk_tile(const PeerRows& peers, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                      float* coefs, float* entropy, cudaStream_t s) {
+    if (K <= 4) topk_tile_launch<4>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 8) topk_tile_launch<8>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 16) topk_tile_launch<16>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else topk_tile_launch<32>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
 }
 
 void launch_topk_peers(const PeerRows& peers, int64_t first_row, int64_t rows, int64_t valid_rows, int L, int K,
                        uint32_t* atoms, float* coefs, cudaStream_t s) {
     if (rows <= 0) return;
-    const unsigned g = grid_for(rows, 128);
-    if (K <= 4) topk_peers_kernel<4><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
-    else if (K <= 8) topk_peers_kernel<8><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
-    else if (K <= 16) topk_peers_kernel<16><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
-    else topk_peers_kernel<32><<<g, 128, 0, s>>>(peers, first_row, rows, valid_rows, L, K, atoms, coefs);
+    PeerRows pr = peers;
+    for (int q = 0; q < pr.n; q++) pr.W[q] = peers.W[q] + first_row * (int64_t)L;
+    topk_tile(pr, rows, valid_rows, L, K, atoms, coefs, nullptr, s);  // (the caller checked L % 4, alignment)
 }
 
 template <int KMAX>
-static void topk_dispatch(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
-                          float* coefs, float* entropy, cudaStream_t s) {
-    if (L % 4 == 0 && (reinterpret_cast<uintptr_t>(W) % 16) == 0)
-        topk_kernel<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs, entropy);
-    else
-        topk_kernel_scalar<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs,
-                                                                     entropy);
+static void topk_dispatch_scalar(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                                 float* coefs, float* entropy, cudaStream_t s) {
+    topk_kernel_scalar<KMAX><<<grid_for(rows, 128), 128, 0, s>>>(W, rows, valid_rows, L, K, atoms, coefs, entropy);
 }
 
 void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms, float* coefs,
                  float* entropy, cudaStream_t s) {
     if (rows <= 0) return;
-    if (K <= 4) topk_dispatch<4>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else if (K <= 8) topk_dispatch<8>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else if (K <= 16) topk_dispatch<16>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else topk_dispatch<32>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    if (L % 4 == 0 && (reinterpret_cast<uintptr_t>(W) % 16) == 0) {
+        PeerRows pr{};
+        pr.W[0] = W;
+        pr.n = 1;
+        topk_tile(pr, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+        return;
+    }
+    if (K <= 4) topk_dispatch_scalar<4>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 8) topk_dispatch_scalar<8>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 16) topk_dispatch_scalar<16>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else topk_dispatch_scalar<32>(W, rows, valid_rows, L, K, atoms, coefs, entropy, s);
 }
 
 }  // namespace scoup

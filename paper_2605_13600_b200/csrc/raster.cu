@@ -148,6 +148,7 @@ struct __align__(16) Smem {
     unsigned long long contrib;
     unsigned long long tests;
     unsigned long long evals;
+    unsigned long long reds;
 };
 
 
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             key[l] = rid;
         }
     }
-    if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; sm.evals = 0ull; }
+    if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; sm.evals = 0ull; sm.reds = 0ull; }
     if (t < MAX_SLOTS) sm.slot_key[t][0] = SLOT_EMPTY;
     for (int i = t; i < 3 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
     if (t < 3 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
     // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
     float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
-    uint32_t cnt = 0, tests = 0, wevals = 0;
+    uint32_t cnt = 0, tests = 0, wevals = 0, nred = 0;
     const int L = p.L;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                     a = sm.slot_atom[q][ls];
                     c = sm.slot_coef[q][ls];
                 }
+                if (COUNT && v > 0.f && a != NONE) nred++;
                 if (v > 0.f && a != NONE)
                     atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
                               __fmul_rn(c, v));
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             }
             if (t < BATCH) {
                 const float z = sm.accZ[buf][t];
+                if (COUNT && z > 0.f) nred++;
                 if (z > 0.f) atomicAdd(p.Z + __float_as_uint(q2[q_head + t].z), z);
             }
             // zero the buffer of batch i+2 (flushed in batch i-1, before this batch's barrier)
@@ -572,6 +575,8 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const unsigned ts = __reduce_add_sync(FULL, tests);
         if (lane == 0 && ts) atomicAdd(&sm.tests, (unsigned long long)ts);
         if (lane == 0 && wevals) atomicAdd(&sm.evals, 32ull * wevals);
+        const unsigned rs = __reduce_add_sync(FULL, nred);
+        if (lane == 0 && rs) atomicAdd(&sm.reds, (unsigned long long)rs);
     }
     __syncthreads();
     if (t == 0) {
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         }
         if (COUNT && sm.tests) atomicAdd(p.support_ctr, sm.tests);
         if (COUNT && sm.evals) atomicAdd(p.lane_eval_ctr, sm.evals);
+        if (COUNT && sm.reds) atomicAdd(p.red_ctr, sm.reds);
     }
 }
 

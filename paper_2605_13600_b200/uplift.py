@@ -128,6 +128,11 @@ class SparseUplift:
     def set_counters(self, enable: bool = True):
         abi.scoup_uplift_set_counters(self._h, enable)
 
+    def set_pipeline(self, contexts: int = 2):
+        """1: every batch step in order on one stream (per-kernel event times = each kernel's own
+        duration); 2 (default): two overlapping pipeline contexts."""
+        abi.scoup_uplift_set_pipeline(self._h, contexts)
+
     def set_timing(self, enable: bool = True):
         abi.scoup_uplift_set_timing(self._h, enable)
 

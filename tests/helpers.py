@@ -45,6 +45,41 @@ def compare_accumulators(W_gpu, Z_gpu, W_ora, Z_ora, rtol=1e-4, atol=1e-6):
 
 
 def compare_codes(atoms_gpu, coefs_gpu, W_ora, K, rtol=1e-4, atol=1e-6):
+    """compare_codes_rows (below) with a vectorised fast path: rows whose GPU atom set equals the
+    oracle's positive Top-K set (oracle.topk: value desc, atom asc) are checked with array
+    operations (same coefficient, order and padding rules); every other row goes through the
+    row-by-row comparator, which decides tie exchanges."""
+    import oracle
+    W_ora = np.ascontiguousarray(W_ora, np.float64)
+    G, L = W_ora.shape
+    A = np.asarray(atoms_gpu).astype(np.int64) & 0xFFFFFFFF
+    Cg = np.asarray(coefs_gpu, np.float64)
+    Ao = oracle.topk(W_ora, K)[0].astype(np.int64)
+    valid = A != NONE
+    n_g = valid.sum(1)
+    prefix = np.all(valid == (np.arange(K)[None, :] < n_g[:, None]), axis=1)
+    same = np.all(np.sort(A, 1) == np.sort(Ao, 1), axis=1) & prefix
+    Sg = np.sort(np.where(valid, A, NONE), 1)
+    distinct = ~np.any((Sg[:, 1:] == Sg[:, :-1]) & (Sg[:, 1:] != NONE), axis=1)
+    idx = np.where(valid, A, 0)
+    w = np.take_along_axis(W_ora, idx, 1) * valid
+    denom = w.sum(1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ref = np.where(valid, w / np.where(denom > 0, denom, 1.0)[:, None], 0.0)
+    coef_ok = np.all(np.where(valid, np.abs(Cg - ref) <= atol + rtol * ref, Cg == 0), axis=1)
+    desc = np.all((Cg[:, :-1] >= Cg[:, 1:]) | ~valid[:, 1:], axis=1) if K > 1 else np.ones(G, bool)
+    fast = same & distinct & coef_ok & desc
+    slow = np.where(~fast)[0]
+    bad, ties, worst = 0, 0, ""
+    if len(slow):
+        b, t, wst = compare_codes_rows(A[slow], Cg[slow], W_ora[slow], K, rtol, atol)
+        bad, ties, worst = b, t, wst
+        if wst:
+            worst = f"(row index within the non-fast rows, first of {len(slow)}) " + wst
+    return bad, ties, worst
+
+
+def compare_codes_rows(atoms_gpu, coefs_gpu, W_ora, K, rtol=1e-4, atol=1e-6):
     """SURVEY.md §8(c) comparator, step 3.  Returns (n_mismatch, n_tie_allowance, worst_msg).
 
     The GPU's atom set must equal the oracle's positive-Top-K set, except that atoms whose

@@ -10,7 +10,7 @@ import pytest
 from paper_2605_13600_b200 import abi, build
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("scoup.h", "scoup_sparse_coding.h")]
+HEADERS = [os.path.join(ROOT, "include", h) for h in sorted(os.listdir(os.path.join(ROOT, "include"))) if h.endswith(".h")]
 
 
 @pytest.fixture(scope="module")

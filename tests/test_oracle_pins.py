@@ -212,6 +212,43 @@ def test_two_overlapping_off_centre_closed_form():
     assert checked >= 4
 
 
+def test_rotated_anisotropic_per_pixel_alpha():
+    """Eq. 2 alpha = o exp(-1/2 d^T Sigma_2D^-1 d) per pixel for one ROTATED anisotropic
+    Gaussian (SURVEY F2 geometry: s = (0.3, 0.15, 0.2), 30 deg about the optical axis), against an
+    independent fp64 Sigma_2D (scipy rotation, finite-difference Jacobian).  Off-axis pixels in
+    all four quadrants: the mirrored pixels (dx, dy) and (dx, -dy) have different alphas only
+    through the cross term b dx dy of the conic, so a flipped or dropped cross term (qb in the
+    oracle's log2-domain quadratic form) fails here -- the footprint-sum pin cannot see it."""
+    W = H = 128
+    mu, s = [0.0, 0.0, 2.0], [0.3, 0.15, 0.2]
+    th = math.radians(15.0)
+    q = [math.cos(th), 0.0, 0.0, math.sin(th)]
+    o = 0.25
+    g = gaussians([mu], [s], [q], [o])
+    cam = identity_camera(W, H, 100.0)
+    T, pix, gid, e = oracle.render_view(g, cam)
+    frag = {int(p): float(v) for p, v in zip(pix, e)}
+    S2, m2, _ = _sigma2d_fp64(mu, s, q, cam)
+    Sinv = np.linalg.inv(S2)
+    assert abs(S2[0, 1]) > 0.2 * math.sqrt(S2[0, 0] * S2[1, 1])  # a strongly rotated ellipse
+    checked = 0
+    for ax, ay in [(6, 4), (11, 3), (4, 9), (14, 8), (9, 13)]:
+        vals = {}
+        for sx in (1, -1):
+            for sy in (1, -1):
+                x, y = int(m2[0]) + sx * ax, int(m2[1]) + sy * ay
+                d = np.array([x + 0.5 - m2[0], y + 0.5 - m2[1]])
+                ref = o * math.exp(-0.5 * d @ Sinv @ d)
+                assert ref >= 1.5 / 255  # far from the alpha cut-off: a fragment on both sides
+                got = frag[y * W + x]
+                assert abs(got / ref - 1) < 1e-5, (x, y, got, ref)
+                vals[(sx, sy)] = ref
+                checked += 1
+        # the mirror images differ by far more than the tolerance (the cross term matters)
+        assert abs(vals[(1, 1)] / vals[(1, -1)] - 1) > 0.05
+    assert checked == 20
+
+
 def test_termination_reading():
     """DESIGN.md §4 reading R9 (3DGS): a fragment whose T(1-alpha) < 1e-4 ends the pixel
     without contributing.  Three coincident o = 0.99 Gaussians: only the front one contributes."""
