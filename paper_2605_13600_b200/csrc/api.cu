@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/scoup.h"
@@ -102,8 +103,10 @@ void grow(T** ptr, size_t* cap, size_t need, cudaStream_t s, double slack = 1.25
 enum Step : int { ST_IDLE = 0, ST_NEAR_FRONT, ST_NEAR_RASTER, ST_FAR_FRONT, ST_FAR_RASTER };
 
 struct Ctx {
-    cudaStream_t s = nullptr;
+    cudaStream_t s = nullptr;     // the batch's steps (high priority: the front's short kernels)
+    cudaStream_t rs = nullptr;    // its raster launches (low priority), joined back into s
     cudaEvent_t ev = nullptr;     // end of the last enqueued step (the host waits on it)
+    cudaEvent_t ev_rs0 = nullptr, ev_rs1 = nullptr;  // s -> rs -> s hand-offs around a raster
     ViewBuffers vb{};
     size_t g_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0;
     void* cub_tmp = nullptr;
@@ -209,8 +212,16 @@ scoup_status check_latched(scoup_uplift* h) {
 }
 
 void ctx_init(Ctx& c) {
-    CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+    // stream priorities: while one context's raster fills the GPU, the other context's front
+    // kernels (depth pass, selections, sorts, emission) are scheduled ahead of the raster's
+    // pending CTAs as SMs free up, so the front runs in the raster's shadow
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&c.s, cudaStreamNonBlocking, greatest));
+    CK(cudaStreamCreateWithPriority(&c.rs, cudaStreamNonBlocking, least));
     CK(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_rs0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_rs1, cudaEventDisableTiming));
     CK(cudaMallocHost((void**)&c.h_hist, sizeof(uint32_t) * MAX_VB * NHIST));
     CK(cudaMallocHost((void**)&c.h_thr, sizeof(uint32_t) * MAX_VB));
     CK(cudaMallocHost((void**)&c.h_total, sizeof(uint64_t)));
@@ -231,6 +242,12 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     for (void* p : hp)
         if (p) cudaFreeHost(p);
     if (c.ev) cudaEventDestroy(c.ev);
+    if (c.ev_rs0) cudaEventDestroy(c.ev_rs0);
+    if (c.ev_rs1) cudaEventDestroy(c.ev_rs1);
+    if (c.rs) {
+        cudaStreamSynchronize(c.rs);
+        cudaStreamDestroy(c.rs);
+    }
     if (c.s) cudaStreamDestroy(c.s);
     c = Ctx{};
 }
@@ -331,8 +348,8 @@ Ctx::EvSet* ev_begin(scoup_uplift* h, Ctx& c) {
     return &es;
 }
 
-void ev_mark(Ctx& c, int k) {
-    if (c.ev_cur >= 0) CK(cudaEventRecord(c.evs[c.ev_cur].e[k], c.s));
+void ev_mark(Ctx& c, int k, cudaStream_t st = nullptr) {
+    if (c.ev_cur >= 0) CK(cudaEventRecord(c.evs[c.ev_cur].e[k], st ? st : c.s));
 }
 
 // Bins: squares of 2^bin_shift px (default 64x64, SCOUP_BIN_SHIFT) holding the depth-ordered
@@ -574,10 +591,15 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.lane_eval_ctr = h->d_stats + 5;
     p.red_ctr = h->d_stats + 2;
     p.err = latch_of(h);
-    ev_mark(c, mark0);
-    if (a.render) launch_render(p, c.s);
-    else launch_raster(p, c.s);
-    ev_mark(c, mark0 + 1);
+    // the raster on the context's low-priority stream, joined back before the next step
+    CK(cudaEventRecord(c.ev_rs0, c.s));
+    CK(cudaStreamWaitEvent(c.rs, c.ev_rs0, 0));
+    ev_mark(c, mark0, c.rs);
+    if (a.render) launch_render(p, c.rs);
+    else launch_raster(p, c.rs);
+    ev_mark(c, mark0 + 1, c.rs);
+    CK(cudaEventRecord(c.ev_rs1, c.rs));
+    CK(cudaStreamWaitEvent(c.s, c.ev_rs1, 0));
     h->kernel_launches += 1;
     return SCOUP_OK;
 }
@@ -698,20 +720,39 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
         };
         scoup_status st = SCOUP_OK;
         for (int ci = 0; ci < 2; ci++) h->ctx[ci].step = ST_IDLE;
-        for (bool busy = true; busy && st == SCOUP_OK;) {
-            busy = false;
+        // Event-driven step machine: a context advances as soon as its last enqueued step has
+        // completed (its next step needs a count read back by the host), independently of the
+        // other context -- so one context can run its whole front (several short steps with host
+        // round trips) while the other's raster runs.  When neither is ready, the host waits.
+        auto advance = [&](int ci) {
+            Ctx& c = h->ctx[ci];
+            switch (c.step) {
+                case ST_IDLE: start_batch(c); h->batches[ci]++; break;
+                case ST_NEAR_FRONT: step_near_front(h, c, args); break;
+                case ST_NEAR_RASTER: st = step_near_raster(h, c, args); break;
+                case ST_FAR_FRONT: step_far_front(h, c, args); break;
+                case ST_FAR_RASTER: st = step_far_raster(h, c, args); break;
+            }
+        };
+        for (;;) {
+            bool any = false, progressed = false;
             for (int ci = 0; ci < h->nctx && st == SCOUP_OK; ci++) {
                 Ctx& c = h->ctx[ci];
-                switch (c.step) {
-                    case ST_IDLE:
-                        if (next < num_views) { start_batch(c); h->batches[ci]++; busy = true; }
-                        break;
-                    case ST_NEAR_FRONT: step_near_front(h, c, args); busy = true; break;
-                    case ST_NEAR_RASTER: st = step_near_raster(h, c, args); busy = true; break;
-                    case ST_FAR_FRONT: step_far_front(h, c, args); busy = true; break;
-                    case ST_FAR_RASTER: st = step_far_raster(h, c, args); busy = true; break;
+                if (c.step == ST_IDLE) {
+                    if (next < num_views) { advance(ci); progressed = true; any = true; }
+                    continue;
+                }
+                any = true;
+                const cudaError_t q = cudaEventQuery(c.ev);
+                if (q == cudaSuccess) {
+                    advance(ci);
+                    progressed = true;
+                } else if (q != cudaErrorNotReady) {
+                    CK(q);
                 }
             }
+            if (st != SCOUP_OK || !any) break;
+            if (!progressed) std::this_thread::yield();
         }
         // ---- join back into the caller's stream
         for (int i = 0; i < 2; i++) {

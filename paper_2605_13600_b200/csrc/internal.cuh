@@ -224,44 +224,42 @@ __device__ __forceinline__ void row_span(const Span& s, int ty, int tiles_x, int
     (void)tiles_x;
 }
 
-// The same x-extent computation with the Span parameters precomputed in preprocess (rec2.w = sy,
-// rec3 = (ky/(-qa), yc/(-qa), -qb/(2 qa), sx), sx < 0: box only): the pixel-centre x-interval
-// [xl, xr] where the Gaussian may produce a fragment within the pixel-centre rows [Y0, Y1]
-// (false: none).  Used by the raster's tile and warp filters (conservative; the exact decision
-// is the per-pixel spec).
-__device__ __forceinline__ bool band_extent(float4 a, float4 e2, float4 e3, float Y0, float Y1, float& xl, float& xr) {
-    const float mx = a.x, my = a.y;
-    if (my + e2.y < Y0 || my - e2.y > Y1) return false;
-    xl = mx - e2.x;
-    xr = mx + e2.x;
-    const float sx = e3.w, sy = e2.w;
-    if (!(sx > 0.f)) return true;
-    const float ey0 = Y0 - 0.5f - my, ey1 = Y1 + 0.5f - my;
-    float rr, ll;
-    if (sy >= ey0 && sy <= ey1) {
-        rr = sx;
-    } else {
-        const float ey = sy < ey0 ? ey0 : ey1;
-        const float h2 = e3.x * ey * ey - e3.y;
-        if (h2 < 0.f) return false;
-        rr = e3.z * ey + sqrtf(h2);
-    }
-    if (-sy >= ey0 && -sy <= ey1) {
-        ll = -sx;
-    } else {
-        const float ey = -sy < ey0 ? ey0 : ey1;
-        const float h2 = e3.x * ey * ey - e3.y;
-        if (h2 < 0.f) return false;
-        ll = e3.z * ey - sqrtf(h2);
-    }
-    xr = fminf(xr, mx + rr + 0.5f + 1e-4f * (fabsf(rr) + fabsf(mx)) + 1e-3f);
-    xl = fmaxf(xl, mx + ll - 0.5f - 1e-4f * (fabsf(ll) + fabsf(mx)) - 1e-3f);
-    return xl <= xr;
+// Hardware square root (MUFU, a few ulp) for the conservative filters below: they only need an
+// upper bound on each chord's extent, so its error is absorbed by an extra outward margin of
+// 1e-6 * h (>> the approximation error) on top of the fp32-rounding margins; unlike IEEE sqrtf it
+// has no slow-path subroutine, so the filter stays in registers.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
+// The same x-extent computation with the Span parameters precomputed in preprocess (rec2.w = sy,
+// rec3 = (ky/(-qa), yc/(-qa), -qb/(2 qa), sx), sx < 0: box only): may the Gaussian produce a
+// fragment at a pixel centre in [X0, X1] x [Y0, Y1]?  Conservative (the exact decision is the
+// per-pixel spec); used by the raster's tile and warp filters.  The right (left) end of the
+// ellipse's x-extent over the row band is at its rightmost (leftmost) point (+-sx, +-sy) when
+// that lies in the band, else at the band edge nearest to it.
 __device__ __forceinline__ bool band_relevant(float4 a, float4 e2, float4 e3, float X0, float X1, float Y0, float Y1) {
-    float xl, xr;
-    return band_extent(a, e2, e3, Y0, Y1, xl, xr) && xr >= X0 && xl <= X1;
+    const float mx = a.x, my = a.y;
+    if (my + e2.y < Y0 || my - e2.y > Y1) return false;
+    float xl = mx - e2.x, xr = mx + e2.x;
+    const float sx = e3.w, sy = e2.w;
+    if (sx > 0.f) {
+        const float ey0 = Y0 - 0.5f - my, ey1 = Y1 + 0.5f - my;
+        // right end: the band edge nearest to the rightmost point (or the point itself)
+        const float eyr = fminf(fmaxf(sy, ey0), ey1), eyl = fminf(fmaxf(-sy, ey0), ey1);
+        const float h2r = e3.x * eyr * eyr - e3.y, h2l = e3.x * eyl * eyl - e3.y;
+        const bool inr = sy >= ey0 && sy <= ey1, inl = -sy >= ey0 && -sy <= ey1;
+        if ((!inr && h2r < 0.f) || (!inl && h2l < 0.f)) return false;  // the band misses the ellipse
+        const float hr = sqrt_approx(fmaxf(h2r, 0.f)), hl = sqrt_approx(fmaxf(h2l, 0.f));
+        const float rr = inr ? sx : e3.z * eyr + hr;
+        const float ll = inl ? -sx : e3.z * eyl - hl;
+        xr = fminf(xr, mx + rr + 0.5f + 1e-4f * (fabsf(rr) + fabsf(mx)) + 1e-6f * hr + 1e-3f);
+        xl = fmaxf(xl, mx + ll - 0.5f - 1e-4f * (fabsf(ll) + fabsf(mx)) - 1e-6f * hl - 1e-3f);
+        if (!(xl <= xr)) return false;
+    }
+    return xr >= X0 && xl <= X1;
 }
 
 // DESIGN.md §3 exp2_spec for ycut <= y <= 0 (the caller's conservative prune guarantees

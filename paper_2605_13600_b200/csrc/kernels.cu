@@ -544,18 +544,44 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
     const int64_t left = valid_rows - r0;
     const int nr = left < (int64_t)R ? (int)left : R;  // rows of this tile to read
     const int t = threadIdx.x;
-    for (int i = t; i < nr * L4; i += R) {
-        const int rr = i / L4, c4 = i - rr * L4;
-        const int64_t g = r0 * L4 + i;  // float4 index in the (contiguous) row block
-        float4 v4 = __ldg(reinterpret_cast<const float4*>(peers.W[0]) + g);
-        for (int q = 1; q < peers.n; q++) {
-            const float4 w4 = __ldg(reinterpret_cast<const float4*>(peers.W[q]) + g);
-            v4.x = __fadd_rn(v4.x, w4.x);
-            v4.y = __fadd_rn(v4.y, w4.y);
-            v4.z = __fadd_rn(v4.z, w4.z);
-            v4.w = __fadd_rn(v4.w, w4.w);
+    const int n4 = nr > 0 ? nr * L4 : 0;
+    const float4* src0 = reinterpret_cast<const float4*>(peers.W[0]) + r0 * L4;  // contiguous row block
+    if (peers.n == 1) {
+        // one partial: asynchronous copies straight into the padded rows (every thread's 16-B
+        // copies in flight at once), then one wait
+        for (int i = t; i < n4; i += R) {
+            const int rr = i / L4, c4 = i - rr * L4;
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(tile + rr * LP + 4 * c4);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src0 + i));
         }
-        *reinterpret_cast<float4*>(tile + rr * LP + 4 * c4) = v4;
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else {
+        // P partials summed in rank order 0..P-1, four float4 columns per thread in flight
+        for (int i0 = t; i0 < n4; i0 += 4 * R) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (i0 + u * R < n4) v[u] = __ldg(src0 + i0 + u * R);
+            for (int q = 1; q < peers.n; q++) {
+                const float4* srcq = reinterpret_cast<const float4*>(peers.W[q]) + r0 * L4;
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (i0 + u * R < n4) {
+                        const float4 w4 = __ldg(srcq + i0 + u * R);
+                        v[u].x = __fadd_rn(v[u].x, w4.x);
+                        v[u].y = __fadd_rn(v[u].y, w4.y);
+                        v[u].z = __fadd_rn(v[u].z, w4.z);
+                        v[u].w = __fadd_rn(v[u].w, w4.w);
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (i0 + u * R < n4) {
+                    const int i = i0 + u * R, rr = i / L4, c4 = i - rr * L4;
+                    *reinterpret_cast<float4*>(tile + rr * LP + 4 * c4) = v[u];
+                }
+        }
     }
     __syncthreads();
     const int64_t r = r0 + t;

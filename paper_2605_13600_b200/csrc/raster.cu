@@ -39,8 +39,13 @@ namespace {
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;   // unassigned or outside the image
 constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // slot-table sentinel
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + BATCH)
+constexpr int QCAP = 512;                     // candidate ring (power of two >= 256 + 3 * SBATCH)
 constexpr int NWARP = TILE_PIX / 32;
+#ifndef RASTER_NSUB
+#define RASTER_NSUB 2                         // sub-batches of BATCH records per barrier
+#endif
+constexpr int NSUB = RASTER_NSUB;
+constexpr int SBATCH = NSUB * BATCH;          // records per super-batch (one barrier, one flush)
 #ifndef RGROUP
 #define RGROUP 8                              // records per warp-uniform branch in the pixel loop (even: pairs)
 #endif
@@ -108,21 +113,22 @@ __device__ __noinline__ void overflow_reds(float* W, float* Z, const uint32_t* a
 }
 
 static_assert(BATCH == 32, "batch = one record per lane (transpose-reduction, flush indexing)");
+static_assert((SBATCH & (SBATCH - 1)) == 0 && SBATCH <= TILE_PIX, "super-batch: a power of two, <= one thread each");
 static_assert(RGROUP % 2 == 0 && BATCH % RGROUP == 0, "records are evaluated in pairs");
 
 struct Ring {
-    // ring of candidate records; slots [0, BATCH) are mirrored at [QCAP, QCAP + BATCH) so a
-    // batch q_head .. q_head + BATCH - 1 is always contiguous
+    // ring of candidate records; sub-batches start at multiples of BATCH, so each one is
+    // contiguous in [0, QCAP)
     // (mx, my, r, o) and (qa, qb, qc, ycut) of records 2i and 2i+1, pair-interleaved so the
     // pixel loop evaluates two records per paired-FP32 instruction (FADD2 / FMUL2 / FFMA2):
     // p0[i] = (mx, mx', my, my'), p1[i] = (r, r', o, o'), p2[i] = (qa, qa', qb, qb'),
     // p3[i] = (qc, qc', ycut, ycut')
-    float4 p0[(QCAP + BATCH) / 2];
-    float4 p1[(QCAP + BATCH) / 2];
-    float4 p2[(QCAP + BATCH) / 2];
-    float4 p3[(QCAP + BATCH) / 2];
-    float4 q2[QCAP + BATCH];     // (support-box half-extents x, y, Gaussian id, sy)
-    float4 q3[QCAP + BATCH];     // band_relevant parameters
+    float4 p0[QCAP / 2];
+    float4 p1[QCAP / 2];
+    float4 p2[QCAP / 2];
+    float4 p3[QCAP / 2];
+    float4 q2[QCAP];     // (support-box half-extents x, y, Gaussian id, sy)
+    float4 q3[QCAP];     // band_relevant parameters
 };
 
 struct __align__(16) Smem {
@@ -133,8 +139,8 @@ struct __align__(16) Smem {
     // per (slot, record) sums of a batch, triple-buffered: batch i accumulates into buffer i % 3,
     // which is flushed after the batch's barrier; buffer (i+2) % 3 is zeroed meanwhile, so a
     // single barrier per batch separates every write from every read
-    float acc[3][MAX_SLOTS * BATCH];
-    float accZ[3][BATCH];
+    float acc[3][MAX_SLOTS * SBATCH];
+    float accZ[3][SBATCH];
     // candidate records of the next refill round, fetched with cp.async one round ahead (slot t
     // is written and read by thread t only)
     float4 st0[TILE_PIX], st1[TILE_PIX], st2[TILE_PIX], st3[TILE_PIX];
@@ -224,8 +230,8 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     }
     if (t == 0) { sm.nslot = 0; sm.nstage = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; sm.evals = 0ull; sm.reds = 0ull; }
     if (t < MAX_SLOTS) sm.slot_key[t][0] = SLOT_EMPTY;
-    for (int i = t; i < 3 * MAX_SLOTS * BATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
-    if (t < 3 * BATCH) (&sm.accZ[0][0])[t] = 0.f;
+    for (int i = t; i < 3 * MAX_SLOTS * SBATCH; i += TILE_PIX) (&sm.acc[0][0])[i] = 0.f;
+    for (int i = t; i < 3 * SBATCH; i += TILE_PIX) (&sm.accZ[0][0])[i] = 0.f;
     unsigned grp = FULL;
 #pragma unroll
     for (int l = 0; l < MAX_LEV; l++)
@@ -332,7 +338,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     int buf = 0;
     while (true) {
         // ---- refill the ring: candidates with their warp masks (stable compaction)
-        while (q_count < (uint32_t)BATCH && cursor < range.y) {
+        while (q_count < (uint32_t)SBATCH && cursor < range.y) {
             const uint32_t idx = cursor + t;
             cp_async_wait_all();  // this round's records (my staging slot)
             const float4 r0 = sm.st0[t], r1 = sm.st1[t], r2 = sm.st2[t], r3 = sm.st3[t];
@@ -357,48 +363,50 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 put_pair_rec(pos, r0, r1);
                 q2[pos] = r2;
                 q3[pos] = r3;
-                if (pos < (uint32_t)BATCH) {
-                    put_pair_rec(pos + QCAP, r0, r1);
-                    q2[pos + QCAP] = r2;
-                    q3[pos + QCAP] = r3;
-                }
             }
             q_count += tot;
             cursor += TILE_PIX;
             __syncthreads();
         }
         if (q_count == 0) break;
-        const uint32_t n = min((uint32_t)BATCH, q_count);
-        if (n < (uint32_t)BATCH) {
-            // the tile's last, partial batch: the ring slots past it hold stale records, which
+        // a super-batch: up to NSUB sub-batches of BATCH records (each starts at a multiple of
+        // BATCH in the ring, so it is contiguous), evaluated back to back by every warp, then ONE
+        // barrier and one flush for all of them
+        const uint32_t n = min((uint32_t)SBATCH, q_count);
+        const int nsub = (int)((n + BATCH - 1) / BATCH);
+        if (n % BATCH) {
+            // the tile's last, partial sub-batch: the ring slots past it hold stale records, which
             // the pixel loop (it evaluates whole record groups without a per-record mask test)
             // must see as empty -- a negative support radius fails every square test
-            if ((uint32_t)t >= n && t < BATCH) {
-                const uint32_t pos = q_head + (uint32_t)t;
+            if ((uint32_t)t >= n && t < nsub * BATCH) {
+                const uint32_t pos = (q_head + (uint32_t)t) & (QCAP - 1);
                 pf1[(pos >> 1) * 4 + (pos & 1)] = -1.0f;
             }
             __syncthreads();
         }
-
-        // ---- per-warp mask of batch records that may touch this warp's 8x4 block
+        bool any_sb = false;
+#pragma unroll 1
+        for (int sb = 0; sb < nsub; sb++) {
+        const uint32_t sh = (q_head + (uint32_t)(sb * BATCH)) & (QCAP - 1);  // sub-batch head
+        const uint32_t nsb = min((uint32_t)BATCH, n - (uint32_t)(sb * BATCH));
+        // ---- per-warp mask of sub-batch records that may touch this warp's 8x4 block
         const bool warp_done = __all_sync(FULL, T == 0.f);
         bool rel = false;
-        if (!warp_done && (uint32_t)lane < n)
-            rel = band_relevant(get_rec0(q_head + lane), q2[q_head + lane], q3[q_head + lane], WX0, WX1, WY0, WY1);
+        if (!warp_done && (uint32_t)lane < nsb)
+            rel = band_relevant(get_rec0(sh + lane), q2[sh + lane], q3[sh + lane], WX0, WX1, WY0, WY1);
         const unsigned mask = __ballot_sync(FULL, rel);
 
-        // ---- rasterise: e[j] for batch record j, in depth order (DESIGN.md §3 PX).
+        // ---- rasterise: e[j] for sub-batch record j, in depth order (DESIGN.md §3 PX).
         // Records go in groups of RGROUP with one warp-uniform branch per group: inside a group
         // there is no control flow, so the T-independent work of the next record (loads, q,
         // exp2_spec) overlaps the T update of the current one.  A record outside the warp's
         // mask is a no-op (its `sq` is false).
         float e[BATCH];
         uint32_t cbits = 0u, tbits = 0u;  // per record: contributed / tested (support square)
-        // batches start at even ring positions (q_head is a multiple of BATCH until the last)
-        const ulonglong2* b0 = reinterpret_cast<const ulonglong2*>(sm.u.r.p0) + (q_head >> 1);
-        const ulonglong2* b1 = reinterpret_cast<const ulonglong2*>(sm.u.r.p1) + (q_head >> 1);
-        const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(sm.u.r.p2) + (q_head >> 1);
-        const ulonglong2* b3 = reinterpret_cast<const ulonglong2*>(sm.u.r.p3) + (q_head >> 1);
+        const ulonglong2* b0 = reinterpret_cast<const ulonglong2*>(sm.u.r.p0) + (sh >> 1);
+        const ulonglong2* b1 = reinterpret_cast<const ulonglong2*>(sm.u.r.p1) + (sh >> 1);
+        const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(sm.u.r.p2) + (sh >> 1);
+        const ulonglong2* b3 = reinterpret_cast<const ulonglong2*>(sm.u.r.p3) + (sh >> 1);
 #pragma unroll
         for (int j = 0; j < BATCH; j++) e[j] = 0.f;
 #pragma unroll
@@ -448,6 +456,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         // (uncounted: the reductions run whenever the warp evaluated a record; all-zero sums add
         // nothing)
         const bool any = COUNT ? cbits != 0u : mask != 0u;
+        any_sb = any_sb || any;
         cnt += __popc(cbits);
         tests += __popc(tbits);
         if (COUNT) {  // records this warp evaluated (whole groups: the branch is per group)
@@ -470,7 +479,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                                     ? (p.code_row0[view][l] + (int64_t)k) * S : -1;
                     }
                     overflow_reds(p.W, p.Z, p.dense ? nullptr : p.code_atoms, p.code_coefs, S, L, nlev, p.W_level_stride,
-                                  __float_as_uint(q2[q_head + j].z), e[j], rw[0], rw[1], rw[2], rw[3]);
+                                  __float_as_uint(q2[sh + j].z), e[j], rw[0], rw[1], rw[2], rw[3]);
                 }
             }
         }
@@ -478,13 +487,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         if (!overflow) {
             // ---- per (warp, slot group) transpose-reduction, then shared accumulation
             if (__any_sync(FULL, any)) {
-                // lane l ends with the group's sum for batch record l
+                // lane l ends with the group's sum for sub-batch record l
                 const bool mine_rel = (mask >> lane) & 1u;
+                const int col = sb * BATCH + lane;  // record column in the super-batch sums
                 if (grp == FULL) {
                     const float v = transpose_reduce<false>(e, true, lane);
                     if (mine_rel && v != 0.f) {
-                        atomicAdd(&sm.acc[buf][slot * BATCH + lane], v);
-                        atomicAdd(&sm.accZ[buf][lane], v);
+                        atomicAdd(&sm.acc[buf][slot * SBATCH + col], v);
+                        atomicAdd(&sm.accZ[buf][col], v);
                     }
                 } else {
                     float zsum = 0.f;
@@ -495,18 +505,21 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                         const int q = __shfl_sync(FULL, slot, l);
                         todo &= ~g2;
                         const float v = transpose_reduce<true>(e, (g2 >> lane) & 1u, lane);
-                        if (mine_rel && v != 0.f) atomicAdd(&sm.acc[buf][q * BATCH + lane], v);
+                        if (mine_rel && v != 0.f) atomicAdd(&sm.acc[buf][q * SBATCH + col], v);
                         zsum += mine_rel ? v : 0.f;
                     }
-                    if (zsum != 0.f) atomicAdd(&sm.accZ[buf][lane], zsum);
+                    if (zsum != 0.f) atomicAdd(&sm.accZ[buf][col], zsum);
                 }
             }
         }
-        // B: the batch's sums are complete; also the termination vote (all pixels finished)
+        }  // sub-batches
+        (void)any_sb;
+        // B: the super-batch's sums are complete; also the termination vote (all pixels finished)
         const int alive = __syncthreads_count(T > 0.f);
         if (!overflow) {
             // ---- flush: nlev*S reds per (slot, Gaussian) into W_level, one per Gaussian into Z
             // one red of W update ls (level l = ls / S, code slot ls % S) of (slot q, record j)
+            auto gid_of = [&](int j) { return __float_as_uint(q2[(q_head + (uint32_t)j) & (QCAP - 1)].z); };
             auto red_one = [&](int q, int j, int ls, float v) {
                 const int l = s_log2 >= 0 ? ls >> s_log2 : (int)__umulhi((uint32_t)ls, s_magic);
                 uint32_t a;
@@ -523,38 +536,40 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 }
                 if (COUNT && v > 0.f && a != NONE) nred++;
                 if (v > 0.f && a != NONE)
-                    atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)__float_as_uint(q2[q_head + j].z) * L + a,
-                              __fmul_rn(c, v));
+                    atomicAdd(p.W + (int64_t)l * p.W_level_stride + (int64_t)gid_of(j) * L + a, __fmul_rn(c, v));
             };
+            const int ncol = nsub * BATCH;  // record columns in use (the rest of each slot row is zero)
             if (ls_log2 >= 0) {
                 // nlev * S a power of two (every single-level BASELINE config): the CTA's threads
                 // sweep all (slot, record, update) items, LS consecutive threads per sum
-                const int nitems = nslot * BATCH * LS;
-                for (int i = t; i < nitems; i += TILE_PIX)
-                    red_one(i >> (ls_log2 + 5), (i >> ls_log2) & (BATCH - 1), i & (LS - 1),
-                            sm.acc[buf][i >> ls_log2]);
+                const int nitems = nslot * SBATCH * LS;
+                for (int i = t; i < nitems; i += TILE_PIX) {
+                    const int u = i >> ls_log2, j = u & (SBATCH - 1);
+                    if (j < ncol) red_one(u / SBATCH, j, i & (LS - 1), sm.acc[buf][u]);
+                }
             } else {
                 // (u = i / LS by multiply-high, exact for i * LS < 2^32: every flush index while
-                // LS <= 2048; BATCH is a power of two.  A per-warp ballot over the (slot, record)
+                // LS <= 2048; SBATCH is a power of two.  A per-warp ballot over the (slot, record)
                 // sums that skips the zero ones was measured slower: indoor 106 -> 128 ms)
-                const int nitems = nslot * BATCH * LS;
+                const int nitems = nslot * SBATCH * LS;
                 for (int i = t; i < nitems; i += TILE_PIX) {
                     const uint32_t u = LS <= 2048 ? __umulhi((uint32_t)i, ls_magic) : (uint32_t)i / (uint32_t)LS;
-                    red_one((int)(u >> 5), (int)(u & (BATCH - 1)), i - (int)u * LS, sm.acc[buf][u]);
+                    const int j = (int)(u & (SBATCH - 1));
+                    if (j < ncol) red_one((int)(u / SBATCH), j, i - (int)u * LS, sm.acc[buf][u]);
                 }
             }
-            if (t < BATCH) {
+            if (t < ncol) {
                 const float z = sm.accZ[buf][t];
                 if (COUNT && z > 0.f) nred++;
-                if (z > 0.f) atomicAdd(p.Z + __float_as_uint(q2[q_head + t].z), z);
+                if (z > 0.f) atomicAdd(p.Z + gid_of(t), z);
             }
-            // zero the buffer of batch i+2 (flushed in batch i-1, before this batch's barrier)
+            // zero the buffer of super-batch i+2 (flushed in super-batch i-1, before this barrier)
             const int bz = buf == 0 ? 2 : buf - 1;
-            for (int i = t; i < nslot * BATCH; i += TILE_PIX) sm.acc[bz][i] = 0.f;
-            if (t < BATCH) sm.accZ[bz][t] = 0.f;
+            for (int i = t; i < nslot * SBATCH; i += TILE_PIX) sm.acc[bz][i] = 0.f;
+            if (t < SBATCH) sm.accZ[bz][t] = 0.f;
         }
-        // (no second barrier: the next refill writes only ring slots past this batch, and the
-        // next batch accumulates into another buffer)
+        // (no second barrier: the next refill writes only ring slots past this super-batch, and
+        // the next super-batch accumulates into another buffer)
         q_head = (q_head + n) & (QCAP - 1);
         q_count -= n;
         buf = buf == 2 ? 0 : buf + 1;

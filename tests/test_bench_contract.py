@@ -72,7 +72,7 @@ def test_two_rank_flow_on_one_device_matches_oracle(tmp_path):
     env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--same-device",
                           "--config", "tiny", "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
-                          "--dump-codes", str(tmp_path)], capture_output=True, text=True, timeout=900, cwd=ROOT,
+                          "--dump-codes", str(tmp_path)], capture_output=True, text=True, timeout=400, cwd=ROOT,
                          env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
