@@ -10,7 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "kernels.cu", "raster.cu", "render.cu", "decode.cu", "sparse_coding.cu", "diag.cu"]
+SOURCES = ["api.cu", "kernels.cu", "raster.cu", "raster2.cu", "render.cu", "decode.cu", "sparse_coding.cu", "diag.cu"]
 HEADERS = ["internal.cuh"]
 LIB = os.path.join(HERE, "libscoup.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -27,7 +27,7 @@ NVCC_FLAGS = [
 # (Eq. 7 render accumulation, Eq. 8 decode, Eq. 4 sparse coding: tolerance-based parity) keep
 # nvcc's default FMA contraction.  (render.cu's per-pixel fragment sequence is written with
 # explicit intrinsics, which contraction never touches.)
-SPEC_TUS = {"api.cu", "kernels.cu", "raster.cu"}
+SPEC_TUS = {"api.cu", "kernels.cu", "raster.cu", "raster2.cu"}
 
 
 def tu_flags(src: str):
@@ -50,9 +50,10 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
-    """Compile libscoup.so (or a variant with extra -D defines into `out`)."""
-    if not force and out == LIB and not defines and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), csrc: str = CSRC) -> str:
+    """Compile libscoup.so (or a variant with extra -D defines, or from another source tree
+    `csrc` -- A/B runs of an earlier revision -- into `out`)."""
+    if not force and out == LIB and not defines and csrc == CSRC and not stale():
         return LIB
     tmp = out + f".tmp{os.getpid()}"
     flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include")]
@@ -61,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     with tempfile.TemporaryDirectory(prefix="scoup_build_") as td:
         def compile_one(src: str) -> str:
             obj = os.path.join(td, os.path.splitext(src)[0] + ".o")
-            cmd = [NVCC, *flags, *tu_flags(src), "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *flags, *tu_flags(src), "-c", os.path.join(csrc, src), "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)

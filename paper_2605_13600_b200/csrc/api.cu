@@ -176,6 +176,7 @@ struct scoup_uplift {
     int bin_shift = 0;                  // bins of 2^bin_shift px squares (0: by image width)
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
     int nctx = 2;                       // pipeline contexts in use (set_pipeline)
+    int raster_kernel = 2;              // 2: two-pixel kernel where supported; 1: raster.cu (SCOUP_RASTER=1, A/B)
     int64_t batches[2] = {0, 0};        // view batches per context (stats)
     int64_t near_frac_changes = 0;      // in-call adaptations of near_frac (stats)
     int64_t host_map_chunks = 0;        // up-front region-map copy chunks (stats)
@@ -596,6 +597,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     CK(cudaStreamWaitEvent(c.rs, c.ev_rs0, 0));
     ev_mark(c, mark0, c.rs);
     if (a.render) launch_render(p, c.rs);
+    else if (h->raster_kernel != 1 && raster2_supported(p)) launch_raster2(p, c.rs);
     else launch_raster(p, c.rs);
     ev_mark(c, mark0 + 1, c.rs);
     CK(cudaEventRecord(c.ev_rs1, c.rs));
@@ -862,6 +864,7 @@ scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num
                 h->near_frac_fixed = true;
             }
         }
+        if (const char* rk = std::getenv("SCOUP_RASTER")) h->raster_kernel = std::atoi(rk) == 1 ? 1 : 2;
         if (const char* bs = std::getenv("SCOUP_BIN_SHIFT")) {
             const int v = std::atoi(bs);
             if (v >= 4 && v <= 10) h->bin_shift = v;

@@ -34,6 +34,14 @@
 
 namespace scoup {
 
+#ifdef RASTER_STATS
+// measurement build only (-DRASTER_STATS): warp/sub-batch statistics of the production kernel
+__device__ unsigned long long g_rstat[16];
+#define RSTAT(i, v) atomicAdd(&g_rstat[i], (unsigned long long)(v))
+#else
+#define RSTAT(i, v) ((void)0)
+#endif
+
 namespace {
 
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;   // unassigned or outside the image
@@ -189,6 +197,27 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         }
         return;
     }
+#ifdef RASTER_STATS
+    if (threadIdx.x == 0) { RSTAT(13, 1); RSTAT(14, range.y - range.x); }
+#endif
+    // software-pipelined candidate fetch: the records of round k+1 are in flight (cp.async)
+    // while round k's batches are evaluated; the list indices are loaded one round further ahead.
+    // The first round is issued before the slot setup, whose region-id and code loads then
+    // overlap its two dependent global latencies (list index, then record).
+    auto prefetch = [&](uint32_t e, bool ok) {
+        const uint32_t es = ok ? e : 0u;
+        cp_async16(&sm.st0[t], p.rec0 + es, ok);
+        cp_async16(&sm.st1[t], p.rec1 + es, ok);
+        cp_async16(&sm.st2[t], p.rec2 + es, ok);
+        cp_async16(&sm.st3[t], p.rec3 + es, ok);
+        cp_async_commit();
+    };
+    uint32_t cursor = range.x;
+    {
+        const bool ok = cursor + t < range.y;
+        prefetch(ok ? __ldg(p.eval + cursor + t) : 0u, ok);
+    }
+    uint32_t e_next = cursor + TILE_PIX + t < range.y ? __ldg(p.eval + cursor + TILE_PIX + t) : 0u;
     const int nlev = NLEV1 ? 1 : p.nlev;
     float* const pf0 = reinterpret_cast<float*>(sm.u.r.p0);
     float* const pf1 = reinterpret_cast<float*>(sm.u.r.p1);
@@ -311,29 +340,14 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
     // only after the barrier of the first refill round)
 
     const float px = __fadd_rn((float)x, 0.5f), py = __fadd_rn((float)y, 0.5f);
-    // transmittance; T == 0 marks a finished pixel (the T(1-alpha) < 1e-4 stop, or outside the
-    // image) -- a real T never drops below 1e-4 (DESIGN.md §4 R9)
+    // transmittance; T < 1e-4 marks a finished pixel (T = 0 outside the image; at the stop of
+    // DESIGN.md §4 R9, T(1 - alpha) < 1e-4, T keeps that product) -- a live pixel's T never drops
+    // below 1e-4, and a finished one can only shrink, so it never passes the stop test again
     float T = !inside ? 0.0f : (p.chunk == 0 ? 1.0f : *Tpix);
     uint32_t cnt = 0, tests = 0, wevals = 0, nred = 0;
     const int L = p.L;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
-    // software-pipelined candidate fetch: the records of round k+1 are in flight (cp.async)
-    // while round k's batches are evaluated; the list indices are loaded one round further ahead
-    auto prefetch = [&](uint32_t e, bool ok) {
-        const uint32_t es = ok ? e : 0u;
-        cp_async16(&sm.st0[t], p.rec0 + es, ok);
-        cp_async16(&sm.st1[t], p.rec1 + es, ok);
-        cp_async16(&sm.st2[t], p.rec2 + es, ok);
-        cp_async16(&sm.st3[t], p.rec3 + es, ok);
-        cp_async_commit();
-    };
-    uint32_t cursor = range.x;
-    {
-        const bool ok = cursor + t < range.y;
-        prefetch(ok ? __ldg(p.eval + cursor + t) : 0u, ok);
-    }
-    uint32_t e_next = cursor + TILE_PIX + t < range.y ? __ldg(p.eval + cursor + TILE_PIX + t) : 0u;
     uint32_t q_head = 0, q_count = 0;
     int buf = 0;
     while (true) {
@@ -366,6 +380,9 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
             }
             q_count += tot;
             cursor += TILE_PIX;
+#ifdef RASTER_STATS
+            if (t == 0) { RSTAT(9, 1); RSTAT(10, tot); }
+#endif
             __syncthreads();
         }
         if (q_count == 0) break;
@@ -374,6 +391,9 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         // barrier and one flush for all of them
         const uint32_t n = min((uint32_t)SBATCH, q_count);
         const int nsub = (int)((n + BATCH - 1) / BATCH);
+#ifdef RASTER_STATS
+        if (t == 0) { RSTAT(11, 1); RSTAT(12, n); }
+#endif
         if (n % BATCH) {
             // the tile's last, partial sub-batch: the ring slots past it hold stale records, which
             // the pixel loop (it evaluates whole record groups without a per-record mask test)
@@ -390,11 +410,22 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         const uint32_t sh = (q_head + (uint32_t)(sb * BATCH)) & (QCAP - 1);  // sub-batch head
         const uint32_t nsb = min((uint32_t)BATCH, n - (uint32_t)(sb * BATCH));
         // ---- per-warp mask of sub-batch records that may touch this warp's 8x4 block
-        const bool warp_done = __all_sync(FULL, T == 0.f);
+        const bool warp_done = __all_sync(FULL, !(T >= K_TMIN));
         bool rel = false;
         if (!warp_done && (uint32_t)lane < nsb)
             rel = band_relevant(get_rec0(sh + lane), q2[sh + lane], q3[sh + lane], WX0, WX1, WY0, WY1);
         const unsigned mask = __ballot_sync(FULL, rel);
+#ifdef RASTER_STATS
+        if (lane == 0 && !warp_done) {
+            int ng = 0;
+            for (int g0 = 0; g0 < BATCH; g0 += RGROUP) ng += ((mask >> g0) & ((1u << RGROUP) - 1u)) ? 1 : 0;
+            RSTAT(0, 1);
+            RSTAT(1 + ng, 1);          // [1..5]: 0..4 active groups
+            RSTAT(6, grp == FULL);
+            RSTAT(7, __popc(mask));
+            RSTAT(8, nsb);
+        }
+#endif
 
         // ---- rasterise: e[j] for sub-batch record j, in depth order (DESIGN.md §3 PX).
         // Records go in groups of RGROUP with one warp-uniform branch per group: inside a group
@@ -436,18 +467,18 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
                 const float dxh = h ? dx1 : dx0, dyh = h ? dy1 : dy0, qh = h ? q1 : q0, rh = h ? r1 : r0;
                 const float yh = h ? y1 : y0, al = h ? al1 : al0, om = h ? om1 : om0;
                 const int jj = j + h;
-                // (a finished pixel, T == 0, needs no test of its own: its Tn = 0 < 1e-4 makes
-                // every later fragment a non-contributing stop that leaves T = 0)
+                // (a finished pixel, T < 1e-4, needs no test of its own: its Tn <= T < 1e-4 makes
+                // every later fragment a non-contributing stop that leaves T < 1e-4)
                 // (the record's warp-mask bit is only needed for the support-test count: a
                 // record outside the mask cannot pass the alpha test anywhere in the block --
                 // band_relevant is conservative -- so it is a no-op for every lane)
                 const bool sq = (!COUNT || ((mask >> jj) & 1u)) && fabsf(dxh) <= rh && fabsf(dyh) <= rh;
-                const bool active = COUNT && T > 0.f;
+                const bool active = COUNT && T >= K_TMIN;
                 const float Tn = __fmul_rn(T, om);
                 const bool pass = sq && !(qh > 0.f) && qh >= yh && al >= K_AMIN;
                 const bool con = pass && !(Tn < K_TMIN);
                 e[jj] = con ? __fmul_rn(al, T) : 0.f;
-                T = con ? Tn : (pass ? 0.f : T);  // pass && !con: the pixel ends here
+                T = pass ? Tn : T;  // pass && !con: the pixel ends here (Tn < 1e-4); a short chain
                 if (COUNT && con) cbits |= 1u << jj;
                 if (COUNT && sq && active) tbits |= 1u << jj;
             }
@@ -515,7 +546,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
         }  // sub-batches
         (void)any_sb;
         // B: the super-batch's sums are complete; also the termination vote (all pixels finished)
-        const int alive = __syncthreads_count(T > 0.f);
+        const int alive = __syncthreads_count(T >= K_TMIN);
         if (!overflow) {
             // ---- flush: nlev*S reds per (slot, Gaussian) into W_level, one per Gaussian into Z
             // one red of W update ls (level l = ls / S, code slot ls % S) of (slot q, record j)
@@ -580,7 +611,7 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 
     // carry the per-pixel state to the next chunk
     if (inside) *Tpix = T;
-    const int live = __syncthreads_count(T > 0.f);
+    const int live = __syncthreads_count(T >= K_TMIN);
     if (t == 0) p.tile_live[gtile] = live > 0 ? 1 : 0;
 
     // contributions (terms of Eq. 5's sum) and support tests
@@ -606,6 +637,18 @@ __global__ void __launch_bounds__(TILE_PIX, RASTER_MIN_BLOCKS) raster_aggregate_
 }
 
 }  // namespace
+
+#ifdef RASTER_STATS
+extern "C" int scoup_debug_raster_stats(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_rstat, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_rstat, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 void launch_raster(const RasterParams& p, cudaStream_t s) {
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
