@@ -36,13 +36,21 @@ constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // slot-table sentinel
 constexpr int R2T = 128;                      // threads per CTA (4 warps, 2 pixels each)
 constexpr int R2W = R2T / 32;
 constexpr int R2Q = 256;                      // ring capacity (>= 63 + 128 records in flight)
-constexpr int R2SB = 64;                      // records per super-batch (2 sub-batches of BATCH)
+#ifndef RASTER2_NSUB
+#define RASTER2_NSUB 2                        // sub-batches of BATCH records per barrier
+#endif
+#ifndef RASTER2_SLOTS
+#define RASTER2_SLOTS 8                       // distinct regions per tile on the shared-sum path (more: per-pixel path)
+#endif
+constexpr int R2SB = RASTER2_NSUB * BATCH;    // records per super-batch (one barrier, one flush)
+constexpr int R2S = RASTER2_SLOTS;
 constexpr int RG = 8;                         // records per warp-uniform group (and per reduction)
 #ifndef RASTER2_MIN_BLOCKS
-#define RASTER2_MIN_BLOCKS 5
+#define RASTER2_MIN_BLOCKS 6
 #endif
 
-static_assert(BATCH == 32 && R2SB == 2 * BATCH, "two sub-batches of one record per lane");
+static_assert(BATCH == 32 && (R2SB & (R2SB - 1)) == 0 && R2SB <= R2T, "sub-batches of one record per lane");
+static_assert(R2S <= MAX_SLOTS, "slot table");
 static_assert(R2Q >= R2SB - 1 + R2T, "ring holds a round on top of a partial super-batch");
 
 struct __align__(16) R2Smem {
@@ -54,16 +62,16 @@ struct __align__(16) R2Smem {
     // primary slot (its lowest) in its own row accw (plain stores -- sm_100 has no native
     // shared-memory FP32 atomic add, atomicAdd there is a CAS loop), its other slots in acc
     // (CAS atomics; warps with more than one slot are the minority)
-    float acc[3][MAX_SLOTS * R2SB];
+    float acc[3][R2S * R2SB];
     float accw[3][R2W][R2SB];
     int wslot[R2W];
     float4 st0[R2T], st1[R2T], st2[R2T], st3[R2T];  // next round's candidates (cp.async staging)
-    uint32_t slot_key[MAX_SLOTS];
-    uint32_t slot_atom[MAX_SLOTS][MAX_S];
-    float slot_coef[MAX_SLOTS][MAX_S];
+    uint32_t slot_key[R2S];
+    uint32_t slot_atom[R2S][MAX_S];
+    float slot_coef[R2S][MAX_S];
     int nslot;
     int overflow;
-    int wcnt[R2W];
+    int wcnt[2][R2W];  // accepted candidates per warp, double-buffered over refill rounds
     unsigned long long contrib, tests, evals, reds;
 };
 
@@ -178,8 +186,8 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
     };
     const uint32_t kA = region(inA, yA), kB = region(inB, yB);
     if (t == 0) { sm.nslot = 0; sm.overflow = 0; sm.contrib = 0ull; sm.tests = 0ull; sm.evals = 0ull; sm.reds = 0ull; }
-    if (t < MAX_SLOTS) sm.slot_key[t] = SLOT_EMPTY;
-    for (int i = t; i < 3 * MAX_SLOTS * R2SB; i += R2T) (&sm.acc[0][0])[i] = 0.f;
+    if (t < R2S) sm.slot_key[t] = SLOT_EMPTY;
+    for (int i = t; i < 3 * R2S * R2SB; i += R2T) (&sm.acc[0][0])[i] = 0.f;
     for (int i = t; i < 3 * R2W * R2SB; i += R2T) (&sm.accw[0][0][0])[i] = 0.f;
     __syncthreads();
     // one claim per distinct key per warp (CAS: the first empty or matching slot)
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
         const int leader = __ffs(g) - 1;
         int sl = -1;
         if (lane == leader) {
-            for (int q = 0; q < MAX_SLOTS; q++) {
+            for (int q = 0; q < R2S; q++) {
                 const uint32_t old = atomicCAS(&sm.slot_key[q], SLOT_EMPTY, k);
                 if (old == SLOT_EMPTY || old == k) { sl = q; break; }
             }
@@ -233,9 +241,12 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
     uint32_t cnt = 0, tests = 0, wevals = 0, nred = 0;
     const unsigned lanemask_lt = (1u << lane) - 1u;
     uint32_t q_head = 0, q_count = 0;
-    int buf = 0;
+    int buf = 0, rbuf = 0;
     while (true) {
-        // ---- refill the ring (stable compaction of the round's accepted candidates)
+        // ---- refill the ring (stable compaction of the round's accepted candidates).  One
+        // barrier per round (the per-warp counts are double-buffered, so the next round's counts
+        // never overwrite ones still being read) and one after the last round's ring writes.
+        bool refilled = false;
         while (q_count < (uint32_t)R2SB && cursor < range.y) {
             const uint32_t idx = cursor + t;
             cp_async_wait_all();
@@ -247,12 +258,12 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                 e_next = nidx + R2T < range.y ? __ldg(p.eval + nidx + R2T) : 0u;
             }
             const unsigned bal = __ballot_sync(FULL, acc);
-            if (lane == 0) sm.wcnt[warp] = __popc(bal);
+            if (lane == 0) sm.wcnt[rbuf][warp] = __popc(bal);
             __syncthreads();
             uint32_t off = 0, tot = 0;
 #pragma unroll
             for (int w = 0; w < R2W; w++) {
-                const uint32_t c = (uint32_t)sm.wcnt[w];
+                const uint32_t c = (uint32_t)sm.wcnt[rbuf][w];
                 off += (w < warp) ? c : 0u;
                 tot += c;
             }
@@ -265,8 +276,10 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
             }
             q_count += tot;
             cursor += R2T;
-            __syncthreads();
+            rbuf ^= 1;
+            refilled = true;
         }
+        if (refilled) __syncthreads();
         if (q_count == 0) break;
         const uint32_t n = min((uint32_t)R2SB, q_count);
         const int nsub = (int)((n + BATCH - 1) / BATCH);
@@ -372,6 +385,9 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
         // the super-batch's sums are complete; termination vote (all pixels finished)
         const int alive = __syncthreads_count(TA >= K_TMIN || TB >= K_TMIN);
         if (!overflow) {
+            int ws[R2W];  // the warps' primary slots (their sums are in accw)
+#pragma unroll
+            for (int w = 0; w < R2W; w++) ws[w] = sm.wslot[w];
             // ---- flush: S reds per (slot, record) into W, one per record into Z (sum over slots)
             const int ncol = nsub * BATCH;
             auto gid_of = [&](int j) { return __float_as_uint(sm.re[(q_head + (uint32_t)j) & (R2Q - 1)].z); };
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                 float v = sm.acc[buf][u];
 #pragma unroll
                 for (int w = 0; w < R2W; w++)
-                    if (sm.wslot[w] == q) v += sm.accw[buf][w][j];
+                    if (ws[w] == q) v += sm.accw[buf][w][j];
                 const uint32_t a = sm.slot_atom[q][s];
                 if (v > 0.f && a != NONE) {
                     if (COUNT) nred++;
