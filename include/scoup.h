@@ -87,6 +87,7 @@ typedef struct {
     double near_frac;       /* the near-chunk fraction now in use */
     int64_t global_reds;    /* red.global.add.f32 issued by the fused kernel's flush into W and Z
                                (lane level; counted with the support tests) */
+    int64_t view_batch;     /* views per pipeline batch (the library's batch size) */
 } scoup_stats;
 
 /* Per-kernel-class device time (CUDA events on the launching streams), accumulated while

@@ -37,7 +37,7 @@ class scoup_stats(C.Structure):
                 ("visible", C.c_int64), ("support_tests", C.c_int64), ("kernel_launches", C.c_int64),
                 ("cub_launches", C.c_int64), ("lane_evaluations", C.c_int64), ("batches", C.c_int64 * 2),
                 ("near_frac_changes", C.c_int64), ("host_map_chunks", C.c_int64), ("near_frac", C.c_double),
-                ("global_reds", C.c_int64)]
+                ("global_reds", C.c_int64), ("view_batch", C.c_int64)]
 
 
 class scoup_timing(C.Structure):

@@ -108,7 +108,7 @@ struct Ctx {
     cudaEvent_t ev = nullptr;     // end of the last enqueued step (the host waits on it)
     cudaEvent_t ev_rs0 = nullptr, ev_rs1 = nullptr;  // s -> rs -> s hand-offs around a raster
     ViewBuffers vb{};
-    size_t g_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0;
+    size_t g_cap = 0, s_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_cap = 0;
     // pinned host staging
@@ -236,8 +236,8 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     c.evs.clear();
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.code, b.hist, b.thr, b.cams, b.sel, b.nsel, b.skey, b.skey_alt, b.sval, b.sval_sorted,
-                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.flags, b.live_sat, b.Tstate, b.tile_live, b.ekey, b.eval,
-                    b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp};
+                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.flags, b.trect, b.selcnt, b.live_sat, b.Tstate,
+                    b.tile_live, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp};
     for (void* p : ptrs) dfree(p, s);
     void* hp[] = {c.h_hist, c.h_thr, c.h_total, c.h_nsel, c.h_cams};
     for (void* p : hp)
@@ -255,19 +255,34 @@ void ctx_free(Ctx& c, cudaStream_t s) {
 
 void ctx_reserve_cub(Ctx& c, size_t bytes) { grow((char**)&c.cub_tmp, &c.cub_cap, bytes, c.s); }
 
-// Per-(view, Gaussian) buffers for batches of up to n = B*G elements, per-pixel state for
-// B views of npx pixels, tile flags for B*ntiles tiles.
-void ctx_reserve(Ctx& c, int64_t n, int64_t pixels, int64_t tiles) {
+// Per-selected-element buffers (EWA records, sort keys, bin counts) for a chunk of n elements:
+// grown on demand (stream-ordered on the context's stream, after every earlier reader).
+void ctx_reserve_sel(Ctx& c, int64_t n) {
     ViewBuffers& b = c.vb;
     n = std::max<int64_t>(n, 1);
+    if ((size_t)n <= c.s_cap && b.rec0) return;
+    const size_t cap = (size_t)((double)n * 1.25);
+    void* ptrs[] = {b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.offsets, b.rect,
+                    b.rec0, b.rec1, b.rec2, b.rec3};
+    for (void* p : ptrs) dfree(p, c.s);
+#define RG(f) { dalloc(&b.f, cap, c.s); }
+    RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1) RG(rec2) RG(rec3)
+#undef RG
+    c.s_cap = cap;
+}
+
+// Per-(view, Gaussian) buffers for batches of up to B*G elements, per-pixel state for
+// B views of npx pixels, tile flags for B*ntiles tiles.
+void ctx_reserve(Ctx& c, int64_t G, int B, int64_t pixels, int64_t tiles) {
+    ViewBuffers& b = c.vb;
+    const int64_t n = std::max<int64_t>((int64_t)B * G, 1);
     if ((size_t)n > c.g_cap || !b.code) {
-        void* ptrs[] = {b.code, b.sel, b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.offsets, b.rect,
-                        b.rec0, b.rec1, b.rec2, b.rec3, b.flags};
+        void* ptrs[] = {b.code, b.sel, b.flags, b.trect, b.selcnt};
         for (void* p : ptrs) dfree(p, c.s);
 #define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
-        RG(code) RG(sel) RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0)
-        RG(rec1) RG(rec2) RG(rec3) RG(flags)
+        RG(code) RG(sel) RG(flags) RG(trect)
 #undef RG
+        dalloc(&b.selcnt, select_counts_needed(G, MAX_VB) + 1, c.s);
         c.g_cap = (size_t)n;
     }
     if (!b.hist) {
@@ -425,7 +440,7 @@ void step_depth(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     *c.h_cams = c.cams;
     CK(cudaMemcpyAsync(b.cams, c.h_cams, sizeof(CamBatch), cudaMemcpyHostToDevice, c.s));
     CK(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * NHIST * c.nv, c.s));
-    launch_depth_pass(h->pg, h->G, c.cams, c.key_bits, b.code, b.hist, h->d_stats + 3, latch_of(h), c.s);
+    launch_depth_pass(h->pg, h->G, c.cams, c.key_bits, b.code, b.hist, h->d_stats + 3, latch_of(h), a.bn, b.trect, c.s);
     CK(cudaMemcpyAsync(c.h_hist, b.hist, sizeof(uint32_t) * NHIST * c.nv, cudaMemcpyDeviceToHost, c.s));
     CK(cudaEventRecord(c.ev, c.s));
     h->kernel_launches += 1;
@@ -438,6 +453,7 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
     ViewBuffers& b = c.vb;
     c.nsel = nsel;
     if (nsel <= 0) return;
+    ctx_reserve_sel(c, nsel);
     int vbits = 0;
     while ((1 << vbits) < c.nv) vbits++;
     const int end_bit = c.key_bits + vbits;
@@ -491,10 +507,8 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     ViewBuffers& b = c.vb;
     CK(cudaMemcpyAsync(b.thr, c.h_thr, sizeof(uint32_t) * c.nv, cudaMemcpyHostToDevice, c.s));
     if (n0 > 0) {
-        const size_t need = select_temp_bytes((int64_t)c.nv * h->G);
-        ctx_reserve_cub(c, need);
-        launch_select_near(b, h->G, c.nv, c.key_bits, c.cub_tmp, c.cub_cap, c.s);
-        h->cub_launches += 1;
+        launch_select_near2(b, h->G, c.nv, c.key_bits, b.selcnt, c.s);
+        h->kernel_launches += 3;
     }
     chunk_front(h, c, a, n0);
     ev_mark(c, 1);
@@ -613,13 +627,9 @@ scoup_status step_near_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     scoup_status st = chunk_back(h, c, a, 0, 2);
     if (st != SCOUP_OK) return st;
     if (c.far_any) {
-        const size_t need = select_temp_bytes((int64_t)c.nv * h->G);
-        ctx_reserve_cub(c, need);
-        launch_far_flags(c.vb, h->pg, h->G, c.cams, c.key_bits, a.bn, c.vb.flags, c.s);
-        launch_select_flagged(c.vb, c.vb.flags, (int64_t)c.nv * h->G, c.cub_tmp, c.cub_cap, c.s);
-        h->kernel_launches += 2;
+        launch_select_far2(c.vb, h->pg, h->G, c.nv, c.key_bits, a.bn, c.vb.selcnt, c.s);
+        h->kernel_launches += 4;
         CK(cudaMemcpyAsync(c.h_nsel, c.vb.nsel, sizeof(int), cudaMemcpyDeviceToHost, c.s));
-        h->cub_launches += 1;
     }
     CK(cudaEventRecord(c.ev, c.s));
     c.step = ST_FAR_FRONT;
@@ -670,7 +680,7 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
         CK(cudaEventRecord(h->ev_fork, h->stream));
         for (int i = 0; i < 2; i++) {
             CK(cudaStreamWaitEvent(h->ctx[i].s, h->ev_fork, 0));
-            ctx_reserve(h->ctx[i], (int64_t)Bmax * h->G, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
+            ctx_reserve(h->ctx[i], h->G, Bmax, (int64_t)Bmax * npx, (int64_t)Bmax * ntiles);
         }
         args.cams = cams.data();
         if (!ids_on_device && nlev > 0) {
@@ -1323,6 +1333,7 @@ scoup_status scoup_uplift_get_stats(scoup_uplift* h, scoup_stats* out) {
         out->cub_launches = h->cub_launches;
         out->lane_evaluations = (int64_t)s[5];
         out->global_reds = (int64_t)s[2];
+        out->view_batch = MAX_VB;
         out->batches[0] = h->batches[0];
         out->batches[1] = h->batches[1];
         out->near_frac_changes = h->near_frac_changes;

@@ -16,7 +16,10 @@ constexpr int TILE_PIX = TILE * TILE;
 constexpr int BATCH = 32;                // Gaussians staged per raster batch
 constexpr int MAX_SLOTS = 16;            // distinct region(-tuple)s per tile on the smem-aggregated path
 constexpr int MAX_S = 16;
-constexpr int MAX_VB = 8;                // views batched per preprocess/sort/raster pass
+#ifndef SCOUP_MAX_VB
+#define SCOUP_MAX_VB 16
+#endif
+constexpr int MAX_VB = SCOUP_MAX_VB;     // views batched per preprocess/sort/raster pass
 constexpr int MAX_LEV = 4;               // semantic levels fused per raster pass (nlev * S <= MAX_S)
 constexpr int MAX_SAT_ENTRIES = 12288;   // (tiles_x + 1) * (tiles_y + 1): 1920x1080 needs 121 x 69
 constexpr int HIST_BITS = 10;            // depth-code histogram resolution (near/far split)
@@ -85,6 +88,9 @@ struct ViewBuffers {
     float* Tstate;           // [B*H*W] per-pixel transmittance between chunks (0 = finished)
     uint8_t* tile_live;      // [B*tiles] 1 while a tile has an unfinished pixel
     uint8_t* flags;          // [B*G] far-chunk selection flags
+    uint32_t* selcnt;        // tile counts / offsets of the stable compactions
+    uint32_t* trect;         // [B*G] conservative reach box in 16x16 tiles (x0, x1, y0, y1: 8 bits each),
+                             //       written by the depth pass for the far-chunk predicate
     uint32_t* live_sat;      // [B*(tiles_x+1)*(tiles_y+1)] summed-area table of tile_live
     uint32_t* ekey;          // [E] v*nbins + bin of each (Gaussian, bin) entry
     uint32_t* eval;          // [E] batch index j
@@ -374,7 +380,8 @@ void launch_activate(const float* means, const float* scales, const float* rots,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);
 void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s);
 void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* code,
-                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, cudaStream_t s);
+                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
+                       uint32_t* trect, cudaStream_t s);
 // stable compactions into vb.sel / vb.nsel; temp storage grown through *tmp / *tmp_bytes
 size_t select_temp_bytes(int64_t n);
 void launch_select_near(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, void* tmp, size_t tmp_bytes,
@@ -389,6 +396,12 @@ void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int k
                  const ViewBuffers& vb, const Binning& bn, int width, int height, int64_t n, int nviews,
                  uint32_t* ekey, uint32_t* eval, cudaStream_t s);
 void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s);
+// custom stable compactions (kernels.cu): near / far chunk selections into vb.sel, count into
+// vb.nsel; counts = scratch of select_counts_needed(G, nviews) tile counts
+size_t select_counts_needed(int64_t G, int nviews);
+void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, uint32_t* counts, cudaStream_t s);
+void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
+                        const Binning& bn, uint32_t* counts, cudaStream_t s);
 void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
                       const Binning& bn, uint8_t* flags, cudaStream_t s);
 void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s);

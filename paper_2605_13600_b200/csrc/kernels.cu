@@ -6,6 +6,7 @@
 //   ranges          per-tile [begin, end) of the tile-sorted entries
 //   ingest_codes    Algorithm 1's per-pixel TopK(W_v(p)) realised per region
 //   topk            Eq. 6 Top-K + L1 renormalisation (Algorithm 1)
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -128,16 +129,21 @@ __device__ __forceinline__ void camera_space(const float4& A, const Camera& cam,
 // lambda_max(Sigma_3D) = s_max^2 and ||J W||_2 <= ||J||_F, the square support r of V7 is at most
 // 3 sqrt(s_max^2 ||J||_F^2 + 0.3); padded for fp32 rounding.  mean2d is computed with the exact
 // V3 operations, so it equals preprocess's.
-__device__ __forceinline__ void reach(const float t[3], float s2max, const Camera& cam, float& mx, float& my,
-                                      float& rb) {
-    const float u = dv(t[0], t[2]), v = dv(t[1], t[2]);
-    mx = add(mul(cam.fx, u), cam.cx);
-    my = add(mul(cam.fy, v), cam.cy);
-    const float iz = 1.0f / t[2];
+// The same bound with hardware reciprocal / square root (the depth pass's hot path): their few-ulp
+// errors move mean2d by < 1e-6 |fx u| px and the radius by < 1e-6 relative, inside the bound's
+// 0.2% + 1 px padding, which a second 1e-5 |fx u| + 1e-5 |fy v| term widens further.
+__device__ __forceinline__ void reach_fast(const float t[3], float s2max, const Camera& cam, float& mx, float& my,
+                                           float& rb) {
+    const float iz = __fdividef(1.0f, t[2]);
+    const float u = t[0] * iz, v = t[1] * iz;
+    const float fu = cam.fx * u, fv = cam.fy * v;
+    mx = fu + cam.cx;
+    my = fv + cam.cy;
     const float jf2 = (cam.fx * cam.fx * (1.0f + u * u) + cam.fy * cam.fy * (1.0f + v * v)) * iz * iz;
-    rb = 3.0f * sqrtf(s2max * jf2 + K_LOWPASS) * 1.002f + 1.0f;
+    float sq;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(s2max * jf2 + K_LOWPASS));
+    rb = 3.0f * sq * 1.002f + 1.0f + 1e-5f * (fabsf(fu) + fabsf(fv));
 }
-
 __device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const Camera& cam) {
     return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height &&
            isfinite(mx) && isfinite(my) && isfinite(rb);
@@ -150,10 +156,24 @@ __device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const
 // shared histogram and the visible count are flushed to global memory once per block.
 constexpr int ITEMS_PER_THREAD = 16;
 
+// Packed reach box in 16x16 tiles for the far-chunk predicate (x0 | x1 << 8 | y0 << 16 | y1 << 24;
+// x0 > x1: no tile); images up to 255 tiles a side (wider ones recompute in far_flags).
+constexpr uint32_t TRECT_EMPTY = 0x000000FFu;
+__device__ __forceinline__ uint32_t tile_rect(float mx, float my, float rb, int tiles_x, int tiles_y) {
+    // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
+    const int x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
+    const int x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
+    const int y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
+    const int y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+    if (x0 > x1 || y0 > y1) return TRECT_EMPTY;
+    return (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
+}
+
 __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
                                                          int key_bits, uint32_t* __restrict__ code,
                                                          uint32_t* __restrict__ hist, unsigned long long* visible_ctr,
-                                                         ErrorLatch err) {
+                                                         ErrorLatch err, int tiles_x, int tiles_y,
+                                                         uint32_t* __restrict__ trect) {
     __shared__ uint32_t sh[NHIST];
     __shared__ uint32_t svis;
     for (int k = threadIdx.x; k < NHIST; k += blockDim.x) sh[k] = 0;
@@ -165,18 +185,19 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
     const int shift = key_bits > HIST_BITS ? key_bits - HIST_BITS : 0;
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
     uint32_t nvis = 0;
+#pragma unroll 4
     for (int it = 0; it < ITEMS_PER_THREAD; it++) {
         const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
         bool vis = false;
         int bucket = -1;
         if (i < G) {
             const float4 A = pg.a[i];
-            uint32_t c = none;
+            uint32_t c = none, rect = TRECT_EMPTY;
             float t[3];
             camera_space(A, cam, t);
             if (t[2] > K_NEAR && A.w >= K_AMIN) {
                 float mx, my, rb;
-                reach(t, pg.s2[i], cam, mx, my, rb);
+                reach_fast(t, pg.s2[i], cam, mx, my, rb);
                 if (box_on_image(mx, my, rb, cam)) {
                     c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
                     vis = c < none;
@@ -184,12 +205,15 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
                         latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + i);
                         c = none;
                     }
+                    if (trect) rect = tile_rect(mx, my, rb, tiles_x, tiles_y);
                 }
             }
             code[(int64_t)view * G + i] = c;
+            if (trect) trect[(int64_t)view * G + i] = rect;
             bucket = vis ? (int)(c >> shift) : -1;
         }
-        // warp-aggregated histogram: one shared atomic per distinct bucket in the warp
+        // warp-aggregated histogram: one shared atomic per distinct bucket in the warp (the depth
+        // codes of a scene concentrate in few buckets: plain per-lane atomics contend)
         const unsigned peers = __match_any_sync(0xffffffffu, bucket);
         if (bucket >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bucket], (uint32_t)__popc(peers));
         nvis += vis ? 1u : 0u;
@@ -247,13 +271,15 @@ __global__ void __launch_bounds__(256) far_flags_kernel(PackedGaussians pg, int6
                                                         const uint32_t* __restrict__ code,
                                                         const uint32_t* __restrict__ thr, uint32_t none,
                                                         const uint32_t* __restrict__ sat, int tiles_x,
-                                                        int tiles_y, uint8_t* __restrict__ flags) {
+                                                        int tiles_y, const uint32_t* __restrict__ trect,
+                                                        uint8_t* __restrict__ flags) {
     const int view = blockIdx.y;
     const int W1 = tiles_x + 1;
     const uint32_t* S = sat + (int64_t)view * W1 * (tiles_y + 1);
     const Camera& cam = cams.cam[view];
     const uint32_t tv = thr[view];
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
+#pragma unroll 4
     for (int it = 0; it < ITEMS_PER_THREAD; it++) {
         const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
         if (i >= G) break;
@@ -261,15 +287,21 @@ __global__ void __launch_bounds__(256) far_flags_kernel(PackedGaussians pg, int6
         const uint32_t c = code[j];
         bool keep = false;
         if (c != none && c >= tv) {
-            float t[3];
-            camera_space(pg.a[i], cam, t);
-            float mx, my, rb;
-            reach(t, pg.s2[i], cam, mx, my, rb);
-            // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
-            const int x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
-            const int x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
-            const int y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
-            const int y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+            int x0, x1, y0, y1;
+            if (trect) {  // the depth pass's packed box
+                const uint32_t r = trect[j];
+                x0 = (int)(r & 255u); x1 = (int)((r >> 8) & 255u); y0 = (int)((r >> 16) & 255u); y1 = (int)(r >> 24);
+            } else {      // (images wider or taller than 255 tiles) recompute the bound
+                float t[3];
+                camera_space(pg.a[i], cam, t);
+                float mx, my, rb;
+                reach_fast(t, pg.s2[i], cam, mx, my, rb);
+                // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
+                x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
+                x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
+                y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
+                y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+            }
             if (x0 <= x1 && y0 <= y1) {
                 const uint32_t n = __ldg(S + (y1 + 1) * W1 + x1 + 1) - __ldg(S + y0 * W1 + x1 + 1) -
                                    __ldg(S + (y1 + 1) * W1 + x0) + __ldg(S + y0 * W1 + x0);
@@ -278,6 +310,176 @@ __global__ void __launch_bounds__(256) far_flags_kernel(PackedGaussians pg, int6
         }
         flags[j] = keep ? 1 : 0;
     }
+}
+
+// ------------------------------------------------------------------ stable compaction
+// The chunk selections as one stable compaction over the batch indices j = v * G + i (index order
+// kept, so equal depth codes keep index order through the stable depth sort):
+// count per 4096-element tile -> exclusive scan of the tile counts (one CTA) -> scatter.  Each
+// warp owns 512 consecutive elements of its tile (16 rounds of 32), so ranks are ballot prefix
+// sums in order.  Predicates: the near chunk (code below the view's split), the far chunk (code
+// at or beyond the split and the conservative reach box covering a live tile).
+constexpr int SEL_ITEMS = 16;
+constexpr int SEL_TILE = 256 * SEL_ITEMS;
+
+struct NearSel {
+    static constexpr bool kStageSat = false;
+    const uint32_t* ssat = nullptr;
+    const uint32_t* sat = nullptr;
+    int tiles_x = 0, tiles_y = 0;
+    const uint32_t* code;
+    const uint32_t* thr;
+    int64_t G;
+    uint32_t none;
+    __device__ __forceinline__ uint2 load(int view, int64_t i) const {
+        return make_uint2(code[(int64_t)view * G + i], 0u);
+    }
+    __device__ __forceinline__ bool test(int view, int64_t i, uint2 v) const { return v.x < thr[view] && v.x != none; }
+};
+
+struct FarSel {
+    const uint32_t* code;
+    const uint32_t* thr;
+    int64_t G;
+    uint32_t none;
+    const uint32_t* trect;   // packed boxes from the depth pass, or NULL: recompute
+    const uint32_t* sat;     // live-tile summed-area tables
+    int tiles_x, tiles_y;
+    PackedGaussians pg;
+    const CamBatch* cams;    // device copy (recompute path)
+    // both words loaded unconditionally (coalesced; the branch-free loads of a thread's items
+    // can all be in flight at once)
+    __device__ __forceinline__ uint2 load(int view, int64_t i) const {
+        const int64_t j = (int64_t)view * G + i;
+        return make_uint2(code[j], trect ? trect[j] : 0u);
+    }
+    __device__ __forceinline__ bool test(int view, int64_t i, uint2 v) const {
+        const uint32_t c = v.x;
+        if (c == none || c < thr[view]) return false;
+        int x0, x1, y0, y1;
+        if (trect) {
+            const uint32_t r = v.y;
+            x0 = (int)(r & 255u); x1 = (int)((r >> 8) & 255u); y0 = (int)((r >> 16) & 255u); y1 = (int)(r >> 24);
+        } else {
+            const Camera& cam = cams->cam[view];
+            float t[3];
+            camera_space(pg.a[i], cam, t);
+            float mx, my, rb;
+            reach_fast(t, pg.s2[i], cam, mx, my, rb);
+            x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
+            x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
+            y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
+            y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+        }
+        if (x0 > x1 || y0 > y1) return false;
+        const int W1 = tiles_x + 1;
+        const uint32_t* S = ssat;  // the view's table, staged in shared memory by the kernel
+        const uint32_t n = S[(y1 + 1) * W1 + x1 + 1] - S[y0 * W1 + x1 + 1] - S[(y1 + 1) * W1 + x0] + S[y0 * W1 + x0];
+        return n > 0;
+    }
+    const uint32_t* ssat = nullptr;
+    static constexpr bool kStageSat = true;
+};
+
+// Blocks stride over the tiles of their view (gridDim.x blocks per view), so the far predicate's
+// table is staged into shared memory once per block, not once per tile.
+template <class Pred>
+__global__ void __launch_bounds__(256) sel_count_kernel(Pred pred, int64_t G, int tiles_per_view,
+                                                        uint32_t* __restrict__ counts, uint32_t* __restrict__ bits) {
+    __shared__ uint32_t ws[2][8];
+    extern __shared__ uint32_t sat_sh[];  // the far predicate's live-tile table of this view
+    const int view = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (Pred::kStageSat) {
+        const int n = (pred.tiles_x + 1) * (pred.tiles_y + 1);
+        const uint32_t* S = pred.sat + (int64_t)view * n;
+        for (int k = threadIdx.x; k < n; k += blockDim.x) sat_sh[k] = S[k];
+        pred.ssat = sat_sh;
+        __syncthreads();
+    }
+    int pb = 0;
+    for (int tl = blockIdx.x; tl < tiles_per_view; tl += gridDim.x, pb ^= 1) {
+        const int64_t base = (int64_t)tl * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
+        const int64_t tile = (int64_t)view * tiles_per_view + tl;
+        uint32_t n = 0, word = 0;
+        uint2 v[SEL_ITEMS];
+#pragma unroll
+        for (int it = 0; it < SEL_ITEMS; it++) {  // every load of the tile first
+            const int64_t i = base + it * 32;
+            v[it] = i < G ? pred.load(view, i) : make_uint2(0xFFFFFFFFu, 0u);
+        }
+#pragma unroll
+        for (int it = 0; it < SEL_ITEMS; it++) {
+            const int64_t i = base + it * 32;
+            const unsigned b = __ballot_sync(0xffffffffu, i < G && pred.test(view, i, v[it]));
+            n += __popc(b);
+            if (lane == it) word = b;  // the warp's 16 predicate words, one per lane, for the scatter
+        }
+        if (lane < SEL_ITEMS) bits[(tile * 8 + warp) * SEL_ITEMS + lane] = word;
+        if (lane == 0) ws[pb][warp] = n;  // (double-buffered: one barrier per tile)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) tot += ws[pb][w];
+            counts[tile] = tot;
+        }
+    }
+}
+
+// exclusive scan of n tile counts in place (one CTA of 1024 threads, n <= 1024 * 64); total -> *nsel
+__global__ void __launch_bounds__(1024) sel_scan_kernel(uint32_t* __restrict__ counts, int n, int* __restrict__ nsel) {
+    typedef cub::BlockScan<uint32_t, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const int per = (n + 1023) / 1024;
+    const int b0 = min(n, threadIdx.x * per), b1 = min(n, b0 + per);
+    uint32_t sum = 0;
+    for (int k = b0; k < b1; k++) sum += counts[k];
+    uint32_t off, total;
+    Scan(tmp).ExclusiveSum(sum, off, total);
+    for (int k = b0; k < b1; k++) {
+        const uint32_t c = counts[k];
+        counts[k] = off;
+        off += c;
+    }
+    if (threadIdx.x == 0) *nsel = (int)total;
+}
+
+// scatter from the count pass's predicate words (no second evaluation of the predicate)
+__global__ void __launch_bounds__(256) sel_scatter_kernel(int64_t G, const uint32_t* __restrict__ offsets,
+                                                          const uint32_t* __restrict__ bits, uint32_t* __restrict__ sel) {
+    __shared__ uint32_t ws[8];
+    const int view = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
+    const int64_t tile = (int64_t)view * gridDim.x + blockIdx.x;
+    const uint32_t word = lane < SEL_ITEMS ? bits[(tile * 8 + warp) * SEL_ITEMS + lane] : 0u;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(word));
+    if (lane == 0) ws[warp] = tot;
+    __syncthreads();
+    uint32_t run = offsets[tile];
+    for (int w = 0; w < warp; w++) run += ws[w];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int it = 0; it < SEL_ITEMS; it++) {
+        const unsigned b = __shfl_sync(0xffffffffu, word, it);
+        if ((b >> lane) & 1u) sel[run + __popc(b & lt)] = (uint32_t)((int64_t)view * G + base + it * 32);
+        run += __popc(b);
+    }
+}
+
+// counts: [tiles] tile counts, then [tiles * 128] predicate words (select_counts_needed)
+template <class Pred>
+static void compact(const Pred& pred, int64_t G, int nviews, uint32_t* counts, uint32_t* sel, int* nsel,
+                    cudaStream_t s) {
+    const dim3 grid(grid_for(G, SEL_TILE), (unsigned)nviews);
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    uint32_t* bits = counts + tiles;
+    const size_t smem = Pred::kStageSat ? sizeof(uint32_t) * (pred.tiles_x + 1) * (pred.tiles_y + 1) : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(sel_count_kernel<Pred>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 cgrid(Pred::kStageSat ? std::min<unsigned>(grid.x, 256u) : grid.x, (unsigned)nviews);
+    sel_count_kernel<Pred><<<cgrid, 256, smem, s>>>(pred, G, (int)grid.x, counts, bits);
+    sel_scan_kernel<<<1, 1024, 0, s>>>(counts, (int)tiles, nsel);
+    sel_scatter_kernel<<<grid, 256, 0, s>>>(G, counts, bits, sel);
 }
 
 // ------------------------------------------------------------------ preprocess (V2-V7)
@@ -690,6 +892,30 @@ __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restric
 
 }  // namespace
 
+size_t select_counts_needed(int64_t G, int nviews) {
+    return (size_t)grid_for(G, SEL_TILE) * (size_t)nviews * (1 + 8 * SEL_ITEMS);
+}
+
+void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, uint32_t* counts, cudaStream_t s) {
+    if (G <= 0 || nviews <= 0) return;
+    NearSel pred;
+    pred.code = vb.code;
+    pred.thr = vb.thr;
+    pred.G = G;
+    pred.none = (1u << key_bits) - 1u;
+    compact(pred, G, nviews, counts, vb.sel, vb.nsel, s);
+}
+
+void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
+                        const Binning& bn, uint32_t* counts, cudaStream_t s) {
+    if (G <= 0 || nviews <= 0) return;
+    live_sat_kernel<<<nviews, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, vb.live_sat);
+    const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
+    const FarSel pred{vb.code, vb.thr, G, (1u << key_bits) - 1u, packed ? vb.trect : nullptr, vb.live_sat,
+                      bn.tiles_x, bn.tiles_y, pg, vb.cams};
+    compact(pred, G, nviews, counts, vb.sel, vb.nsel, s);
+}
+
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac, int64_t G,
                      PackedGaussians pg, ErrorLatch err, cudaStream_t s) {
     if (G <= 0) return;
@@ -703,10 +929,13 @@ void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s) {
 }
 
 void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* code,
-                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, cudaStream_t s) {
+                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
+                       uint32_t* trect, cudaStream_t s) {
     if (G <= 0 || cams.n <= 0) return;
     dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
-    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, code, hist, visible_ctr, err);
+    const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
+    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, code, hist, visible_ctr, err, bn.tiles_x, bn.tiles_y,
+                                           packed ? trect : nullptr);
 }
 
 size_t select_temp_bytes(int64_t n) {
@@ -730,8 +959,9 @@ void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, cons
     if (G <= 0 || cams.n <= 0) return;
     live_sat_kernel<<<cams.n, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, vb.live_sat);
     dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
+    const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
     far_flags_kernel<<<grid, 256, 0, s>>>(pg, G, cams, vb.code, vb.thr, (1u << key_bits) - 1u, vb.live_sat,
-                                          bn.tiles_x, bn.tiles_y, flags);
+                                          bn.tiles_x, bn.tiles_y, packed ? vb.trect : nullptr, flags);
 }
 
 void launch_select_flagged(const ViewBuffers& vb, const uint8_t* flags, int64_t n, void* tmp, size_t tmp_bytes,
