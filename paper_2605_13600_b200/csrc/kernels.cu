@@ -733,7 +733,10 @@ __global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const
 // order 0..P-1 for the fused cross-rank path (peers.n > 1) -- into padded shared rows (stride
 // L + 4 floats: a warp's LDS.128 of one column hits 8 distinct 16-B bank groups per wavefront),
 // then each thread runs the register insertion network on its own row.
-constexpr int TOPK_ROWS = 128;
+#ifndef SCOUP_TOPK_ROWS
+#define SCOUP_TOPK_ROWS 128
+#endif
+constexpr int TOPK_ROWS = SCOUP_TOPK_ROWS;
 
 template <int KMAX>
 __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, int64_t rows, int64_t valid_rows, int L,
@@ -787,7 +790,6 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
     }
     __syncthreads();
     const int64_t r = r0 + t;
-    if (r >= rows) return;
     float bv[KMAX];
     uint32_t ba[KMAX];
     float hs = 0.f, hw = 0.f;  // sum W, sum W ln W
@@ -829,15 +831,40 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
 #pragma unroll
     for (int s = 0; s < KMAX; s++)
         if (s < K) sum = __fadd_rn(sum, bv[s]);
+    if (entropy && r < rows) entropy[r] = hs > 0.f ? fmaxf(0.f, logf(hs) - hw / hs) : __int_as_float(0x7fc00000);
+    if (2 * K > L + 4) {  // (codes wider than half a staged row: direct stores)
+        if (r < rows) {
+#pragma unroll
+            for (int s = 0; s < KMAX; s++) {
+                if (s < K) {
+                    bool keep = bv[s] > 0.f;
+                    atoms[r * K + s] = keep ? ba[s] : NONE;
+                    coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+                }
+            }
+        }
+        return;
+    }
+    // the tile's codes through shared memory (every row has been read: the tile is free), then
+    // one contiguous, coalesced store of its R x K atoms and coefficients
+    __syncthreads();
+    uint32_t* oa = reinterpret_cast<uint32_t*>(tile);
+    float* oc = tile + R * K;
 #pragma unroll
     for (int s = 0; s < KMAX; s++) {
         if (s < K) {
             bool keep = bv[s] > 0.f;
-            atoms[r * K + s] = keep ? ba[s] : NONE;
-            coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+            oa[t * K + s] = keep ? ba[s] : NONE;
+            oc[t * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
         }
     }
-    if (entropy) entropy[r] = hs > 0.f ? fmaxf(0.f, logf(hs) - hw / hs) : __int_as_float(0x7fc00000);
+    __syncthreads();
+    const int64_t left_rows = rows - r0;
+    const int nout = (int)(left_rows < (int64_t)R ? left_rows : (int64_t)R) * K;
+    for (int k = t; k < nout; k += R) {
+        atoms[r0 * K + k] = oa[k];
+        coefs[r0 * K + k] = oc[k];
+    }
 }
 
 // generic L (not a multiple of 4): scalar loads
