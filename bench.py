@@ -483,7 +483,10 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * 128 * sm_max * 1e6 / 1e12  # T lane-ops/s (DESIGN.md §5 a4)
     # algorithmic lane-ops of one step (DESIGN.md §5 a4) over the raster's own time per step
-    ops_step = OPS_PER_TEST * tests_step + (2 * nlev * cfg.S + 1) * contrib_step
+    # (dense features, Eq. 3: the kernel sums e per region slot before the D-wide products, so only
+    # the per-support-test alpha work is counted -- counting 2D + 1 per contribution would exceed
+    # the peak)
+    ops_step = OPS_PER_TEST * tests_step + (0 if dense else (2 * nlev * cfg.S + 1) * contrib_step)
     achieved = ops_step / world / (raster_own_ms / 1e3) / 1e12 if raster_own_ms > 0 else 0.0
     if raster_own_ms > ms_per_step:
         print(f"[bench] WARNING: raster own time {raster_own_ms:.2f} ms > step {ms_per_step:.2f} ms",

@@ -121,6 +121,7 @@ struct Ctx {
     Step step = ST_IDLE;
     int v0 = 0, nv = 0;
     int key_bits = 31;
+    Binning bn{};          // the batch's bins (the adaptive bin size may change between batches)
     int64_t nsel = 0;
     bool far_any = false;
     CamBatch cams{};
@@ -173,7 +174,10 @@ struct scoup_uplift {
     // exact (DESIGN.md §5 a3), so this only moves work between the two chunks.
     double near_frac = 0.05;
     bool near_frac_fixed = false;
-    int bin_shift = 0;                  // bins of 2^bin_shift px squares (0: by image width)
+    int bin_shift = 0;                  // bins of 2^bin_shift px squares fixed by SCOUP_BIN_SHIFT (0: adaptive)
+    int bin_shift_auto = 0;             // adaptive bin size (0: not yet chosen for this image width)
+    int bin_width = 0;                  // image width the adaptive choice was made for
+    int64_t bin_changes = 0;
     bool count_tests = false;           // instrumented raster: contributions + support tests (set_counters)
     int nctx = 2;                       // pipeline contexts in use (set_pipeline)
     int raster_kernel = 2;              // 2: two-pixel kernel where supported; 1: raster.cu (SCOUP_RASTER=1, A/B)
@@ -457,7 +461,7 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
     int vbits = 0;
     while ((1 << vbits) < c.nv) vbits++;
     const int end_bit = c.key_bits + vbits;
-    launch_preprocess(h->pg, h->G, c.cams, a.bn, b, c.key_bits, nsel, c.s);
+    launch_preprocess(h->pg, h->G, c.cams, c.bn, b, c.key_bits, nsel, c.s);
     size_t need = 0, need2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.skey, b.skey_alt, b.sval, b.sval_sorted, (int)nsel, 0, end_bit,
                                        c.s));
@@ -521,7 +525,7 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
 scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, int mark0) {
     ViewBuffers& b = c.vb;
     const uint64_t E = c.nsel > 0 ? *c.h_total : 0;
-    const int ntiles = a.bn.nbins() * c.nv;  // bins of the batch (= the ranges' sentinel key)
+    const int ntiles = c.bn.nbins() * c.nv;  // bins of the batch (= the ranges' sentinel key)
     if (E >= (uint64_t)INT32_MAX)
         return fail(SCOUP_EUNSUPPORTED, "view batch produces " + std::to_string(E) + " tile entries (>= 2^31)");
     if ((size_t)ntiles > c.t_cap || !b.ranges) {
@@ -530,6 +534,22 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
         c.t_cap = ntiles;
     }
     h->host_entries += (int64_t)E;
+    if (chunk == 0 && h->bin_shift == 0 && c.nsel > 0) {
+        // adaptive bin size for later batches: bins covered per near-chunk element.  Large
+        // footprints (many bins each) make the entry sort dominate -> larger bins; small ones
+        // make every tile filter a long list of Gaussians that miss it -> smaller bins
+        // (measured: configs[4] 1570 -> 1145 ms with 128-px instead of 64-px bins; outdoor and
+        // indoor stay at their width-based defaults)
+        const double per = (double)E / (double)c.nsel;
+        const int cur = c.bn.bshx;
+        int nxt = cur;
+        if (per > 12.0 && cur < 8) nxt = cur + 1;
+        else if (per < 1.5 && cur > 5) nxt = cur - 1;
+        if (nxt != cur && nxt != h->bin_shift_auto) {
+            h->bin_shift_auto = nxt;
+            h->bin_changes++;
+        }
+    }
     if (E == 0 && chunk > 0) {
         ev_mark(c, mark0);
         ev_mark(c, mark0 + 1);
@@ -549,7 +569,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
         }
         int vbits = 0;
         while ((1 << vbits) < c.nv) vbits++;
-        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b, a.bn, a.cams[c.v0].width,
+        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b, c.bn, a.cams[c.v0].width,
                     a.cams[c.v0].height, c.nsel, c.nv, b.ekey, b.eval, c.s);
         const int nbits = bits_for((uint32_t)ntiles + 1u);
         size_t need = 0;
@@ -566,7 +586,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.width = a.cams[c.v0].width;
     p.height = a.cams[c.v0].height;
     p.G = h->G;
-    p.bn = a.bn;
+    p.bn = c.bn;
     p.ranges = b.ranges;
     p.eval = b.eval_alt;
     p.rec0 = b.rec0;
@@ -627,7 +647,7 @@ scoup_status step_near_raster(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     scoup_status st = chunk_back(h, c, a, 0, 2);
     if (st != SCOUP_OK) return st;
     if (c.far_any) {
-        launch_select_far2(c.vb, h->pg, h->G, c.nv, c.key_bits, a.bn, c.vb.selcnt, c.s);
+        launch_select_far2(c.vb, h->pg, h->G, c.nv, c.key_bits, c.bn, c.vb.selcnt, c.s);
         h->kernel_launches += 4;
         CK(cudaMemcpyAsync(c.h_nsel, c.vb.nsel, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     }
@@ -719,6 +739,18 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
             c.nv = B;
             c.key_bits = kb;
             next += B;
+            {   // the batch's bins: fixed (SCOUP_BIN_SHIFT) or the handle's adaptive size
+                const int Wd = cams[c.v0].width, Hd = cams[c.v0].height;
+                if (h->bin_shift > 0) {
+                    c.bn = choose_binning(Wd, Hd, h->bin_shift);
+                } else {
+                    if (h->bin_width != Wd) {
+                        h->bin_width = Wd;
+                        h->bin_shift_auto = choose_binning(Wd, Hd, 0).bshx;
+                    }
+                    c.bn = choose_binning(Wd, Hd, h->bin_shift_auto);
+                }
+            }
             if (!ids_on_device && nlev > 0)  // this batch's chunks of the up-front copy
                 for (int j = c.v0 / MAX_VB; j <= (c.v0 + c.nv - 1) / MAX_VB; j++)
                     CK(cudaStreamWaitEvent(c.s, h->chunk_ev[j], 0));
