@@ -100,7 +100,7 @@ void grow(T** ptr, size_t* cap, size_t need, cudaStream_t s, double slack = 1.25
 // One pipeline context: the buffers of one view batch, the stream it runs on, and where the
 // batch is in its sequence of steps (DESIGN.md §5 a3).  Two contexts alternate, so that while
 // the host waits for one context's counts, the GPU runs the other context's queued work.
-enum Step : int { ST_IDLE = 0, ST_NEAR_FRONT, ST_NEAR_RASTER, ST_FAR_FRONT, ST_FAR_RASTER };
+enum Step : int { ST_IDLE = 0, ST_NEAR_FRONT, ST_NEAR_CHUNK, ST_NEAR_RASTER, ST_FAR_FRONT, ST_FAR_RASTER };
 
 struct Ctx {
     cudaStream_t s = nullptr;     // the batch's steps (high priority: the front's short kernels)
@@ -480,19 +480,22 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
 // boundary of the depth code), stable-compacted, then the chunk front.
 void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     CK(cudaEventSynchronize(c.ev));
+    (void)a;
     const uint32_t none = (1u << c.key_bits) - 1u;
     const int shift = c.key_bits > HIST_BITS ? c.key_bits - HIST_BITS : 0;
-    int64_t n0 = 0;
     c.far_any = false;
     c.far_cand = 0;
     for (int v = 0; v < c.nv; v++) {
+        // the histogram samples every HIST_SAMPLE-th Gaussian: the split follows the sample's
+        // quantile; the exact near count comes back from the compaction (next step)
         const uint32_t* hv = c.h_hist + (int64_t)v * NHIST;
         uint64_t total = 0;
         for (int k = 0; k < NHIST; k++) total += hv[k];
         const uint64_t target = (uint64_t)std::ceil(h->near_frac * (double)total);
         uint32_t thr = none;  // everything visible
-        uint64_t cum = 0;
+        uint64_t cum = total;
         if (target < total) {
+            cum = 0;
             for (int k = 0; k < NHIST; k++) {
                 cum += hv[k];
                 if (cum >= target) {
@@ -500,21 +503,24 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
                     break;
                 }
             }
-        } else {
-            cum = total;
         }
-        if (cum < total) c.far_any = true;
+        if (thr != none) c.far_any = true;  // (unsampled Gaussians may lie beyond the split)
         c.h_thr[v] = thr;
-        n0 += (int64_t)cum;
-        c.far_cand += (int64_t)(total - cum);
+        c.far_cand += (int64_t)(total - cum) * HIST_SAMPLE;
     }
     ViewBuffers& b = c.vb;
     CK(cudaMemcpyAsync(b.thr, c.h_thr, sizeof(uint32_t) * c.nv, cudaMemcpyHostToDevice, c.s));
-    if (n0 > 0) {
-        launch_select_near2(b, h->G, c.nv, c.key_bits, b.selcnt, c.s);
-        h->kernel_launches += 3;
-    }
-    chunk_front(h, c, a, n0);
+    launch_select_near2(b, h->G, c.nv, c.key_bits, b.selcnt, c.s);
+    h->kernel_launches += 3;
+    CK(cudaMemcpyAsync(c.h_nsel, b.nsel, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev, c.s));
+    c.step = ST_NEAR_CHUNK;
+}
+
+// Near chunk front on the exact number of selected elements.
+void step_near_chunk(scoup_uplift* h, Ctx& c, const CallArgs& a) {
+    CK(cudaEventSynchronize(c.ev));
+    chunk_front(h, c, a, (int64_t)*c.h_nsel);
     ev_mark(c, 1);
     CK(cudaEventRecord(c.ev, c.s));
     c.step = ST_NEAR_RASTER;
@@ -773,6 +779,7 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
             switch (c.step) {
                 case ST_IDLE: start_batch(c); h->batches[ci]++; break;
                 case ST_NEAR_FRONT: step_near_front(h, c, args); break;
+                case ST_NEAR_CHUNK: step_near_chunk(h, c, args); break;
                 case ST_NEAR_RASTER: st = step_near_raster(h, c, args); break;
                 case ST_FAR_FRONT: step_far_front(h, c, args); break;
                 case ST_FAR_RASTER: st = step_far_raster(h, c, args); break;

@@ -24,6 +24,7 @@ constexpr int MAX_LEV = 4;               // semantic levels fused per raster pas
 constexpr int MAX_SAT_ENTRIES = 12288;   // (tiles_x + 1) * (tiles_y + 1): 1920x1080 needs 121 x 69
 constexpr int HIST_BITS = 10;            // depth-code histogram resolution (near/far split)
 constexpr int NHIST = 1 << HIST_BITS;
+constexpr int HIST_SAMPLE = 8;           // the depth histogram counts every 8th Gaussian
 
 // DESIGN.md §3 constants (hex-exact fp32)
 #define K_NEAR 0x1.99999ap-3f

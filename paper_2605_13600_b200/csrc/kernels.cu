@@ -144,9 +144,10 @@ __device__ __forceinline__ void reach_fast(const float t[3], float s2max, const 
     asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(s2max * jf2 + K_LOWPASS));
     rb = 3.0f * sq * 1.002f + 1.0f + 1e-5f * (fabsf(fu) + fabsf(fv));
 }
+// (NaN fails every comparison; an infinite mean fails one side; an infinite radius keeps the
+// Gaussian -- conservative, the exact EWA of preprocess decides)
 __device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const Camera& cam) {
-    return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height &&
-           isfinite(mx) && isfinite(my) && isfinite(rb);
+    return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height;
 }
 
 // One thread per (view, Gaussian), grid.y = view.  Writes code[j] (j = v*G + i) and the per-view
@@ -161,10 +162,11 @@ constexpr int ITEMS_PER_THREAD = 16;
 constexpr uint32_t TRECT_EMPTY = 0x000000FFu;
 __device__ __forceinline__ uint32_t tile_rect(float mx, float my, float rb, int tiles_x, int tiles_y) {
     // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
-    const int x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
-    const int x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
-    const int y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
-    const int y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
+    // (cvt.rmi saturates: out-of-range and infinite bounds clamp like the exact floor would)
+    const int x0 = max(0, __float2int_rd((mx - rb - 0.5f) * (1.0f / TILE)));
+    const int x1 = min(tiles_x - 1, __float2int_rd((mx + rb - 0.5f) * (1.0f / TILE)));
+    const int y0 = max(0, __float2int_rd((my - rb - 0.5f) * (1.0f / TILE)));
+    const int y1 = min(tiles_y - 1, __float2int_rd((my + rb - 0.5f) * (1.0f / TILE)));
     if (x0 > x1 || y0 > y1) return TRECT_EMPTY;
     return (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
 }
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
     if (threadIdx.x == 0) svis = 0;
     __syncthreads();
     const int view = blockIdx.y;
-    const Camera& cam = cams.cam[view];
+    const Camera cam = cams.cam[view];  // (a register copy: no per-use parameter loads)
     const uint32_t none = (1u << key_bits) - 1u;
     const int shift = key_bits > HIST_BITS ? key_bits - HIST_BITS : 0;
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
@@ -210,7 +212,9 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
             }
             code[(int64_t)view * G + i] = c;
             if (trect) trect[(int64_t)view * G + i] = rect;
-            bucket = vis ? (int)(c >> shift) : -1;
+            // the split histogram samples every HIST_SAMPLE-th Gaussian (the split is a
+            // heuristic: any threshold is exact; the near count comes from the compaction)
+            bucket = vis && (i & (HIST_SAMPLE - 1)) == 0 ? (int)(c >> shift) : -1;
         }
         // warp-aggregated histogram: one shared atomic per distinct bucket in the warp (the depth
         // codes of a scene concentrate in few buckets: plain per-lane atomics contend)
