@@ -10,7 +10,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "kernels.cu", "raster.cu", "raster2.cu", "render.cu", "decode.cu", "sparse_coding.cu", "diag.cu"]
+SOURCES = ["api.cu", "kernels.cu", "binsort.cu", "raster.cu", "raster2.cu", "render.cu", "decode.cu", "sparse_coding.cu", "diag.cu"]
 HEADERS = ["internal.cuh"]
 LIB = os.path.join(HERE, "libscoup.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

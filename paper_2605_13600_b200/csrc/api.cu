@@ -108,7 +108,7 @@ struct Ctx {
     cudaEvent_t ev = nullptr;     // end of the last enqueued step (the host waits on it)
     cudaEvent_t ev_rs0 = nullptr, ev_rs1 = nullptr;  // s -> rs -> s hand-offs around a raster
     ViewBuffers vb{};
-    size_t g_cap = 0, s_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0;
+    size_t g_cap = 0, s_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0, bc_cap = 0, eb_cap = 0, ee_cap = 0;
     void* cub_tmp = nullptr;
     size_t cub_cap = 0;
     // pinned host staging
@@ -240,8 +240,8 @@ void ctx_free(Ctx& c, cudaStream_t s) {
     c.evs.clear();
     ViewBuffers& b = c.vb;
     void* ptrs[] = {b.code, b.hist, b.thr, b.cams, b.sel, b.nsel, b.skey, b.skey_alt, b.sval, b.sval_sorted,
-                    b.tiles, b.offsets, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.flags, b.trect, b.selcnt, b.live_sat, b.Tstate,
-                    b.tile_live, b.ekey, b.eval, b.ekey_alt, b.eval_alt, b.ranges, c.cub_tmp};
+                    b.tiles, b.rect, b.rec0, b.rec1, b.rec2, b.rec3, b.trect, b.selcnt, b.live_sat, b.Tstate,
+                    b.tile_live, b.eval, b.ranges, b.bcnt, b.ebin, b.eel, b.binfo, c.cub_tmp};
     for (void* p : ptrs) dfree(p, s);
     void* hp[] = {c.h_hist, c.h_thr, c.h_total, c.h_nsel, c.h_cams};
     for (void* p : hp)
@@ -266,11 +266,11 @@ void ctx_reserve_sel(Ctx& c, int64_t n) {
     n = std::max<int64_t>(n, 1);
     if ((size_t)n <= c.s_cap && b.rec0) return;
     const size_t cap = (size_t)((double)n * 1.25);
-    void* ptrs[] = {b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.offsets, b.rect,
+    void* ptrs[] = {b.skey, b.skey_alt, b.sval, b.sval_sorted, b.tiles, b.rect,
                     b.rec0, b.rec1, b.rec2, b.rec3};
     for (void* p : ptrs) dfree(p, c.s);
 #define RG(f) { dalloc(&b.f, cap, c.s); }
-    RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(offsets) RG(rect) RG(rec0) RG(rec1) RG(rec2) RG(rec3)
+    RG(skey) RG(skey_alt) RG(sval) RG(sval_sorted) RG(tiles) RG(rect) RG(rec0) RG(rec1) RG(rec2) RG(rec3)
 #undef RG
     c.s_cap = cap;
 }
@@ -281,10 +281,10 @@ void ctx_reserve(Ctx& c, int64_t G, int B, int64_t pixels, int64_t tiles) {
     ViewBuffers& b = c.vb;
     const int64_t n = std::max<int64_t>((int64_t)B * G, 1);
     if ((size_t)n > c.g_cap || !b.code) {
-        void* ptrs[] = {b.code, b.sel, b.flags, b.trect, b.selcnt};
+        void* ptrs[] = {b.code, b.sel, b.trect, b.selcnt};
         for (void* p : ptrs) dfree(p, c.s);
 #define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
-        RG(code) RG(sel) RG(flags) RG(trect)
+        RG(code) RG(sel) RG(trect)
 #undef RG
         dalloc(&b.selcnt, select_counts_needed(G, MAX_VB) + 1, c.s);
         c.g_cap = (size_t)n;
@@ -329,11 +329,6 @@ Camera to_cam(const scoup_camera& c) {
     return k;
 }
 
-int bits_for(uint32_t n) {
-    int b = 1;
-    while ((1u << b) < n && b < 32) b++;
-    return b;
-}
 
 constexpr int EV_RING = 8;
 
@@ -451,9 +446,10 @@ void step_depth(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     c.step = ST_NEAR_FRONT;
 }
 
-// Front of one chunk on the nsel selected elements: EWA preprocess, depth sort, bin-count scan,
-// entry total -> host.
+// Front of one chunk on the nsel selected elements: EWA preprocess, depth sort, per-segment bin
+// counts of the bin scatter (binsort.cu), entry total -> host.
 void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
+    (void)a;
     ViewBuffers& b = c.vb;
     c.nsel = nsel;
     if (nsel <= 0) return;
@@ -462,16 +458,21 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
     while ((1 << vbits) < c.nv) vbits++;
     const int end_bit = c.key_bits + vbits;
     launch_preprocess(h->pg, h->G, c.cams, c.bn, b, c.key_bits, nsel, c.s);
-    size_t need = 0, need2 = 0;
+    size_t need = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.skey, b.skey_alt, b.sval, b.sval_sorted, (int)nsel, 0, end_bit,
                                        c.s));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.offsets, b.offsets, (int)nsel, c.s));
-    ctx_reserve_cub(c, std::max(need, need2));
+    ctx_reserve_cub(c, need);
     CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.skey, b.skey_alt, b.sval, b.sval_sorted, (int)nsel, 0,
                                        end_bit, c.s));
-    launch_gather_scan_input(b.sval_sorted, b.tiles, b.offsets, nsel, c.s);
-    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.offsets, b.offsets, (int)nsel, c.s));
-    CK(cudaMemcpyAsync(c.h_total, b.offsets + (nsel - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
+    // entry counts in sorted order, scanned in place into b.skey (dead after the sort): the
+    // binning's entry offsets; the exact total -> host
+    if (!b.binfo) dalloc(&b.binfo, 1, c.s);
+    launch_binsort_gather(b.sval_sorted, b.tiles, nsel, b.skey, b.binfo, c.s);
+    size_t need2 = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, need2, b.skey, b.skey, (int)nsel, c.s));
+    ctx_reserve_cub(c, need2);
+    CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.skey, b.skey, (int)nsel, c.s));
+    CK(cudaMemcpyAsync(c.h_total, &b.binfo->total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
     h->kernel_launches += 2;
     h->cub_launches += 2;
 }
@@ -561,31 +562,18 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
         ev_mark(c, mark0 + 1);
         return SCOUP_OK;
     }
-    CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * ntiles, c.s));
     if (E > 0) {
-        if (E > c.e_cap || !b.ekey) {
-            size_t ne = (size_t)((double)E * 1.25);
-            void* ptrs[] = {b.ekey, b.eval, b.ekey_alt, b.eval_alt};
-            for (void* p : ptrs) dfree(p, c.s);
-            dalloc(&b.ekey, ne, c.s);
-            dalloc(&b.eval, ne, c.s);
-            dalloc(&b.ekey_alt, ne, c.s);
-            dalloc(&b.eval_alt, ne, c.s);
-            c.e_cap = ne;
-        }
-        int vbits = 0;
-        while ((1 << vbits) < c.nv) vbits++;
-        launch_emit(b.sval_sorted, b.skey_alt, vbits == 0 ? 32 : c.key_bits, b.offsets, b, c.bn, a.cams[c.v0].width,
-                    a.cams[c.v0].height, c.nsel, c.nv, b.ekey, b.eval, c.s);
-        const int nbits = bits_for((uint32_t)ntiles + 1u);
-        size_t need = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits, c.s));
-        ctx_reserve_cub(c, need);
-        CK(cub::DeviceRadixSort::SortPairs(c.cub_tmp, need, b.ekey, b.ekey_alt, b.eval, b.eval_alt, (int)E, 0, nbits,
-                                           c.s));
-        launch_ranges(b.ekey_alt, (int64_t)E, (uint32_t)ntiles, b.ranges, c.s);
-        h->kernel_launches += 2;
-        h->cub_launches += 1;
+        grow(&b.eval, &c.e_cap, (size_t)E, c.s);
+        const int nb = c.bn.nbins();
+        const size_t nseg = binsort_segments_max((int64_t)E, c.nv);
+        grow(&b.bcnt, &c.bc_cap, nseg * (size_t)nb, c.s);
+        grow(&b.ebin, &c.eb_cap, (size_t)E, c.s);
+        grow(&b.eel, &c.ee_cap, (size_t)E, c.s);
+        launch_binsort(b.selcnt, select_tiles_per_view(h->G), b.skey, b.sval_sorted, b.rect, c.nsel, (int64_t)E, c.nv,
+                       c.bn.bins_x, nb, b.binfo, b.bcnt, b.ebin, b.eel, b.ranges, b.eval, c.s);
+        h->kernel_launches += 5;
+    } else {
+        CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * ntiles, c.s));
     }
     RasterParams p{};
     p.nviews = c.nv;
@@ -594,7 +582,7 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     p.G = h->G;
     p.bn = c.bn;
     p.ranges = b.ranges;
-    p.eval = b.eval_alt;
+    p.eval = b.eval;
     p.rec0 = b.rec0;
     p.rec1 = b.rec1;
     p.rec2 = b.rec2;

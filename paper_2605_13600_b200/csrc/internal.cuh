@@ -80,7 +80,6 @@ struct ViewBuffers {
     uint32_t* sval_sorted;   // [B*G] chunk indices in (view, depth, index) order
     // per selected element e of the current chunk (compact, written in sel order):
     uint32_t* tiles;         // bin count of the support rectangle
-    uint64_t* offsets;       // [B*G] inclusive scan of tiles in sorted order
     uint2* rect;             // bin rect (bx0 | by0<<16, bx1 | by1<<16), exclusive ends
     float4* rec0;
     float4* rec1;
@@ -88,18 +87,29 @@ struct ViewBuffers {
     float4* rec3;            // (ky/(-qa), yc/(-qa), -qb/(2 qa), sx): band_relevant parameters
     float* Tstate;           // [B*H*W] per-pixel transmittance between chunks (0 = finished)
     uint8_t* tile_live;      // [B*tiles] 1 while a tile has an unfinished pixel
-    uint8_t* flags;          // [B*G] far-chunk selection flags
     uint32_t* selcnt;        // tile counts / offsets of the stable compactions
     uint32_t* trect;         // [B*G] conservative reach box in 16x16 tiles (x0, x1, y0, y1: 8 bits each),
                              //       written by the depth pass for the far-chunk predicate
     uint32_t* live_sat;      // [B*(tiles_x+1)*(tiles_y+1)] summed-area table of tile_live
-    uint32_t* ekey;          // [E] v*nbins + bin of each (Gaussian, bin) entry
-    uint32_t* eval;          // [E] batch index j
-    uint32_t* ekey_alt;      // [E] sort scratch
-    uint32_t* eval_alt;      // [E]
-    uint2* ranges;           // [B*nbins] [begin, end) into the sorted entries
+    uint32_t* eval;          // [E] chunk element index of each (bin, element) entry, bin lists in depth order
+    uint2* ranges;           // [B*nbins] [begin, end) of each bin's list in eval
+    uint32_t* bcnt;          // [segments * nbins] per-segment bin counts / prefixes (binsort.cu)
+    uint16_t* ebin;          // [E] bin (within the view) of each flattened entry (binsort.cu)
+    uint32_t* eel;           // [E] element of each flattened entry (binsort.cu)
+    struct BsInfo* binfo;    // view starts and segment table of the chunk (binsort.cu)
 };
 
+
+// Segment table of the stable bin scatter (binsort.cu): view v's sorted elements are
+// [vstart[v], vstart[v+1]) and its flattened entries [ebase[v], ebase[v+1]), cut into runs of
+// BS_SEGE entries starting at segment segbase[v].
+constexpr int BS_SEGE = 2048;
+struct BsInfo {
+    uint32_t vstart[MAX_VB + 1];
+    uint32_t ebase[MAX_VB + 1];
+    uint32_t segbase[MAX_VB + 1];
+    unsigned long long total;  // entries of the chunk (exact)
+};
 
 struct ErrorLatch {
     int* code;         // device: 0 = none, else SCOUP_EDATA kind id
@@ -384,27 +394,22 @@ void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int 
                        uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
                        uint32_t* trect, cudaStream_t s);
 // stable compactions into vb.sel / vb.nsel; temp storage grown through *tmp / *tmp_bytes
-size_t select_temp_bytes(int64_t n);
-void launch_select_near(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, void* tmp, size_t tmp_bytes,
-                        cudaStream_t s);
-void launch_select_flagged(const ViewBuffers& vb, const uint8_t* flags, int64_t n, void* tmp, size_t tmp_bytes,
-                           cudaStream_t s);
 void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
                        int key_bits, int64_t nsel, cudaStream_t s);
-void launch_gather_scan_input(const uint32_t* sval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
-                              cudaStream_t s);
-void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int key_bits, const uint64_t* offsets,
-                 const ViewBuffers& vb, const Binning& bn, int width, int height, int64_t n, int nviews,
-                 uint32_t* ekey, uint32_t* eval, cudaStream_t s);
-void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s);
+size_t binsort_segments_max(int64_t entries, int nv);
+void launch_binsort_gather(const uint32_t* sval_sorted, const uint32_t* tiles, int64_t nsel, uint32_t* offs,
+                           BsInfo* info, cudaStream_t s);
+void launch_binsort(const uint32_t* sel_offsets, int tiles_per_view, const uint32_t* offs,
+                    const uint32_t* sval_sorted, const uint2* rect, int64_t nsel, int64_t entries, int nv,
+                    int bins_x, int nb, BsInfo* info, uint32_t* cnt, uint16_t* ebin, uint32_t* eel, uint2* ranges,
+                    uint32_t* eval, cudaStream_t s);
+int select_tiles_per_view(int64_t G);
 // custom stable compactions (kernels.cu): near / far chunk selections into vb.sel, count into
 // vb.nsel; counts = scratch of select_counts_needed(G, nviews) tile counts
 size_t select_counts_needed(int64_t G, int nviews);
 void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, uint32_t* counts, cudaStream_t s);
 void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
                         const Binning& bn, uint32_t* counts, cudaStream_t s);
-void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
-                      const Binning& bn, uint8_t* flags, cudaStream_t s);
 void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s);
 void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_t rows, int S, int K,
                          int L, uint32_t* atoms_out, float* coefs_out, ErrorLatch err, cudaStream_t s);

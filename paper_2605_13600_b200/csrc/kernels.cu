@@ -2,13 +2,11 @@
 //
 //   activate        DESIGN.md §3 G1: q/|q|, R(q), Sigma_3D = R diag(s)^2 R^T
 //   preprocess      DESIGN.md §3 V1-V7: EWA projection, culls, support rect
-//   gather/emit     depth-ordered (Gaussian, tile) entries (3DGS tile binning)
-//   ranges          per-tile [begin, end) of the tile-sorted entries
+//   depth pass, compactions   the depth chunks of a view batch (DESIGN.md §5 a3); the bin lists
+//                   of a chunk are built in binsort.cu
 //   ingest_codes    Algorithm 1's per-pixel TopK(W_v(p)) realised per region
 //   topk            Eq. 6 Top-K + L1 renormalisation (Algorithm 1)
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_select.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include <climits>
 
@@ -233,17 +231,7 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
 // ------------------------------------------------------------------ chunk selection
 // Near chunk of view v: codes below thr[v].  Far chunk: the other visible codes whose
 // conservative reach touches a tile that is still live after the near chunk.  Both are stable
-// compactions (CUB DeviceSelect::If over the batch indices), so index order is kept.
-struct NearPred {
-    const uint32_t* code;
-    const uint32_t* thr;
-    int64_t G;
-    uint32_t none;
-    __device__ __forceinline__ bool operator()(uint32_t j) const {
-        const uint32_t c = code[j];
-        return c < thr[j / G] && c != none;
-    }
-};
+// compactions over the batch indices (below), so index order is kept.
 
 // Summed-area table of the live tiles of each view: sat[v][(ty+1)*(tx_n+1) + tx+1] = number of
 // live tiles in [0, tx] x [0, ty].  One block per view; rows then columns, in shared memory.
@@ -266,54 +254,6 @@ __global__ void __launch_bounds__(1024) live_sat_kernel(const uint8_t* __restric
         for (int y = 1; y < H1; y++) S[y * W1 + x] += S[(y - 1) * W1 + x];
     __syncthreads();
     for (int k = threadIdx.x; k < W1 * H1; k += blockDim.x) sat[(int64_t)v * W1 * H1 + k] = S[k];
-}
-
-// Far flags: one thread per (view, Gaussian) of the far range; kept when its conservative reach
-// box covers a live tile (a fragment needs |x + 0.5 - mean.x| <= r <= rb, same in y), which the
-// summed-area table answers in four loads.
-__global__ void __launch_bounds__(256) far_flags_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
-                                                        const uint32_t* __restrict__ code,
-                                                        const uint32_t* __restrict__ thr, uint32_t none,
-                                                        const uint32_t* __restrict__ sat, int tiles_x,
-                                                        int tiles_y, const uint32_t* __restrict__ trect,
-                                                        uint8_t* __restrict__ flags) {
-    const int view = blockIdx.y;
-    const int W1 = tiles_x + 1;
-    const uint32_t* S = sat + (int64_t)view * W1 * (tiles_y + 1);
-    const Camera& cam = cams.cam[view];
-    const uint32_t tv = thr[view];
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
-#pragma unroll 4
-    for (int it = 0; it < ITEMS_PER_THREAD; it++) {
-        const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
-        if (i >= G) break;
-        const int64_t j = (int64_t)view * G + i;
-        const uint32_t c = code[j];
-        bool keep = false;
-        if (c != none && c >= tv) {
-            int x0, x1, y0, y1;
-            if (trect) {  // the depth pass's packed box
-                const uint32_t r = trect[j];
-                x0 = (int)(r & 255u); x1 = (int)((r >> 8) & 255u); y0 = (int)((r >> 16) & 255u); y1 = (int)(r >> 24);
-            } else {      // (images wider or taller than 255 tiles) recompute the bound
-                float t[3];
-                camera_space(pg.a[i], cam, t);
-                float mx, my, rb;
-                reach_fast(t, pg.s2[i], cam, mx, my, rb);
-                // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
-                x0 = max(0, (int)floorf((mx - rb - 0.5f) * (1.0f / TILE)));
-                x1 = min(tiles_x - 1, (int)floorf((mx + rb - 0.5f) * (1.0f / TILE)));
-                y0 = max(0, (int)floorf((my - rb - 0.5f) * (1.0f / TILE)));
-                y1 = min(tiles_y - 1, (int)floorf((my + rb - 0.5f) * (1.0f / TILE)));
-            }
-            if (x0 <= x1 && y0 <= y1) {
-                const uint32_t n = __ldg(S + (y1 + 1) * W1 + x1 + 1) - __ldg(S + y0 * W1 + x1 + 1) -
-                                   __ldg(S + (y1 + 1) * W1 + x0) + __ldg(S + y0 * W1 + x0);
-                keep = n > 0;
-            }
-        }
-        flags[j] = keep ? 1 : 0;
-    }
 }
 
 // ------------------------------------------------------------------ stable compaction
@@ -603,73 +543,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
     }
 }
 
-__global__ void gather_tiles_kernel(const uint32_t* __restrict__ sval_sorted, const uint32_t* __restrict__ tiles,
-                                    uint64_t* __restrict__ out, int64_t n) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) out[k] = tiles[sval_sorted[k]];
-}
-
-// ------------------------------------------------------------------ emit
-// Entry m of the element at sorted position k (chunk index e, view v = sorted key >> key_bits)
-// goes to slot offsets[k-1] + m: the m-th bin of its support rectangle, keyed v*nbins + bin.
-// The entries are in (view, depth, index) order before the stable bin sort, so each bin's list
-// is too; the raster filters its tile's candidates with band_relevant.
-__global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ sval_sorted,
-                                                   const uint32_t* __restrict__ skey_sorted, int key_bits,
-                                                   const uint64_t* __restrict__ offsets,
-                                                   const uint2* __restrict__ rect, int bins_x, int nbins, int64_t n,
-                                                   uint32_t* __restrict__ ekey, uint32_t* __restrict__ eval) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    uint64_t begin = 0, end = 0;
-    uint32_t g = 0, kbase = 0;
-    uint2 rc = make_uint2(0, 0);
-    if (k < n) {
-        begin = k > 0 ? offsets[k - 1] : 0;
-        end = offsets[k];
-        if (end > begin) {
-            g = sval_sorted[k];
-            rc = rect[g];
-            kbase = (key_bits >= 32 ? 0u : (skey_sorted[k] >> key_bits)) * (uint32_t)nbins;
-        }
-    }
-    const uint32_t cnt = (uint32_t)(end - begin);
-    const uint32_t SMALL = 4;
-    if (cnt > 0 && cnt <= SMALL) {
-        const uint32_t bx0 = rc.x & 0xFFFFu, by0 = rc.x >> 16, w = (rc.y & 0xFFFFu) - bx0;
-        for (uint32_t m = 0; m < cnt; m++) {
-            ekey[begin + m] = kbase + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
-            eval[begin + m] = g;
-        }
-    }
-    unsigned big = __ballot_sync(0xffffffffu, cnt > SMALL);
-    while (big) {
-        const int src = __ffs(big) - 1;
-        big &= big - 1;
-        const uint32_t sg = __shfl_sync(0xffffffffu, g, src);
-        const uint32_t rx = __shfl_sync(0xffffffffu, rc.x, src), ry = __shfl_sync(0xffffffffu, rc.y, src);
-        const uint64_t sb = __shfl_sync(0xffffffffu, begin, src);
-        const uint32_t sc = __shfl_sync(0xffffffffu, cnt, src);
-        const uint32_t skb = __shfl_sync(0xffffffffu, kbase, src);
-        const uint32_t bx0 = rx & 0xFFFFu, by0 = rx >> 16, w = (ry & 0xFFFFu) - bx0;
-        for (uint32_t m = lane; m < sc; m += 32) {
-            ekey[sb + m] = skb + (by0 + m / w) * (uint32_t)bins_x + bx0 + m % w;
-            eval[sb + m] = sg;
-        }
-    }
-}
-
-// Per-bin [begin, end) in the bin-sorted entries (ranges zeroed first; keys >= sentinel skipped).
-__global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t E, uint32_t sentinel,
-                              uint2* __restrict__ ranges) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= E) return;
-    const uint32_t key = keys[k];
-    if (key >= sentinel) return;
-    if (k == 0 || keys[k - 1] != key) ranges[key].x = (uint32_t)k;
-    if (k == E - 1 || keys[k + 1] != key) ranges[key].y = (uint32_t)(k + 1);
-}
-
 // ------------------------------------------------------------------ ingest dense features
 // Dense region features (Eq. 3, the dense-uplift baseline): copy, finite check only.
 __global__ void ingest_dense_kernel(const float* __restrict__ in, int64_t n, float* __restrict__ out, ErrorLatch err) {
@@ -923,6 +796,8 @@ __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restric
 
 }  // namespace
 
+int select_tiles_per_view(int64_t G) { return (int)grid_for(G, SEL_TILE); }
+
 size_t select_counts_needed(int64_t G, int nviews) {
     return (size_t)grid_for(G, SEL_TILE) * (size_t)nviews * (1 + 8 * SEL_ITEMS);
 }
@@ -969,65 +844,11 @@ void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int 
                                            packed ? trect : nullptr);
 }
 
-size_t select_temp_bytes(int64_t n) {
-    size_t a = 0, b = 0;
-    thrust::counting_iterator<uint32_t> it(0);
-    NearPred np{};
-    cub::DeviceSelect::If(nullptr, a, it, (uint32_t*)nullptr, (int*)nullptr, (int)n, np);
-    cub::DeviceSelect::Flagged(nullptr, b, it, (const uint8_t*)nullptr, (uint32_t*)nullptr, (int*)nullptr, (int)n);
-    return std::max(a, b);
-}
-
-void launch_select_near(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, void* tmp, size_t tmp_bytes,
-                        cudaStream_t s) {
-    const int64_t n = (int64_t)nviews * G;
-    NearPred pred{vb.code, vb.thr, G, (1u << key_bits) - 1u};
-    cub::DeviceSelect::If(tmp, tmp_bytes, thrust::counting_iterator<uint32_t>(0), vb.sel, vb.nsel, (int)n, pred, s);
-}
-
-void launch_far_flags(const ViewBuffers& vb, PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits,
-                      const Binning& bn, uint8_t* flags, cudaStream_t s) {
-    if (G <= 0 || cams.n <= 0) return;
-    live_sat_kernel<<<cams.n, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, vb.live_sat);
-    dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
-    const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
-    far_flags_kernel<<<grid, 256, 0, s>>>(pg, G, cams, vb.code, vb.thr, (1u << key_bits) - 1u, vb.live_sat,
-                                          bn.tiles_x, bn.tiles_y, packed ? vb.trect : nullptr, flags);
-}
-
-void launch_select_flagged(const ViewBuffers& vb, const uint8_t* flags, int64_t n, void* tmp, size_t tmp_bytes,
-                           cudaStream_t s) {
-    cub::DeviceSelect::Flagged(tmp, tmp_bytes, thrust::counting_iterator<uint32_t>(0), flags, vb.sel, vb.nsel, (int)n,
-                               s);
-}
-
 void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
                        int key_bits, int64_t nsel, cudaStream_t s) {
     if (nsel <= 0) return;
     preprocess_kernel<<<grid_for(nsel, 256), 256, 0, s>>>(pg, G, cams, bn, vb, key_bits, vb.sel, nsel, vb.skey,
                                                           vb.sval);
-}
-
-void launch_gather_scan_input(const uint32_t* sval_sorted, const uint32_t* tiles, uint64_t* out, int64_t n,
-                              cudaStream_t s) {
-    if (n <= 0) return;
-    gather_tiles_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, tiles, out, n);
-}
-
-void launch_emit(const uint32_t* sval_sorted, const uint32_t* skey_sorted, int key_bits, const uint64_t* offsets,
-                 const ViewBuffers& vb, const Binning& bn, int width, int height, int64_t n, int nviews,
-                 uint32_t* ekey, uint32_t* eval, cudaStream_t s) {
-    if (n <= 0) return;
-    emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(sval_sorted, skey_sorted, key_bits, offsets, vb.rect, bn.bins_x,
-                                                 bn.nbins(), n, ekey, eval);
-    (void)nviews;
-    (void)width;
-    (void)height;
-}
-
-void launch_ranges(const uint32_t* keys_sorted, int64_t E, uint32_t sentinel, uint2* ranges, cudaStream_t s) {
-    if (E <= 0) return;
-    ranges_kernel<<<grid_for(E, 256), 256, 0, s>>>(keys_sorted, E, sentinel, ranges);
 }
 
 void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s) {
