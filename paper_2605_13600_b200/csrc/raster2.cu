@@ -111,6 +111,24 @@ __device__ __forceinline__ float transpose8(float (&v)[RG], int lane) {
     return r;
 }
 
+// alpha if the fragment passes the §3 PX tests (live, |dx| <= r, |dy| <= r, !(q > 0), the
+// conservative q >= ycut, alpha >= 1/255), else 0 -- one predicate chain, one select.
+__device__ __forceinline__ float pass_select(float al, float adx, float ady, float r, float q, float ycut,
+                                             uint32_t live) {
+    float out;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %7, 0;\n\t"
+        "setp.le.and.f32 p, %2, %4, p;\n\t"
+        "setp.le.and.f32 p, %3, %4, p;\n\t"
+        "setp.leu.and.f32 p, %5, 0f00000000, p;\n\t"
+        "setp.ge.and.f32 p, %5, %6, p;\n\t"
+        "setp.ge.and.f32 p, %1, 0f3B808081, p;\n\t"
+        "selp.f32 %0, %1, 0f00000000, p;\n\t}"
+        : "=f"(out)
+        : "f"(al), "f"(adx), "f"(ady), "f"(r), "f"(q), "f"(ycut), "r"(live));
+    return out;
+}
+
 // Fallback aggregation of one fragment (tiles with > MAX_SLOTS regions): the pixel's code and Z.
 __device__ __noinline__ void overflow_red1(float* W, float* Z, const uint32_t* atoms, const float* coefs, int S, int L,
                                            uint32_t g, float ev, int64_t row) {
@@ -319,28 +337,34 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                     const f2 ex = exp2_spec2(q);
                     float mA, mB;
                     f2_split(f2_mul(f2_pack(a.w, a.w), ex), mA, mB);                   // o * exp2_spec(q)
-                    const float alA = fminf(K_ACLAMP, mA), alB = fminf(K_ACLAMP, mB);
-                    const f2 AL = f2_pack(alA, alB);
-                    const f2 T2 = f2_pack(TA, TB);
-                    float TnA, TnB, wA, wB;
-                    f2_split(f2_mul(T2, f2_rsub(AL, 1.0f)), TnA, TnB);                 // T (1 - alpha)
-                    f2_split(f2_mul(AL, T2), wA, wB);                                   // alpha T
                     float dyA, dyB, qA, qB;
                     f2_split(dy, dyA, dyB);
                     f2_split(q, qA, qB);
                     const bool sqx = (!COUNT || ((mask >> (g0 + jj)) & 1u)) && fabsf(dx) <= a.z;
                     const bool sqA = sqx && fabsf(dyA) <= a.z, sqB = sqx && fabsf(dyB) <= a.z;
+                    float alA = fminf(K_ACLAMP, mA), alB = fminf(K_ACLAMP, mB);
                     const bool passA = sqA && !(qA > 0.f) && qA >= b.w && alA >= K_AMIN;
                     const bool passB = sqB && !(qB > 0.f) && qB >= b.w && alB >= K_AMIN;
-                    const bool conA = passA && !(TnA < K_TMIN), conB = passB && !(TnB < K_TMIN);
+                    // a fragment that does not pass takes alpha = 0: T (1 - 0) = T exactly and
+                    // alpha T = 0, so T needs no select (pass && Tn < 1e-4: the pixel ends).  The
+                    // pass test as one predicate chain per pixel and a single select (PTX: the
+                    // compiler otherwise splits the && chain into one select per condition)
+                    alA = pass_select(alA, fabsf(dx), fabsf(dyA), a.z, qA, b.w, COUNT ? ((mask >> (g0 + jj)) & 1u) : 1u);
+                    alB = pass_select(alB, fabsf(dx), fabsf(dyB), a.z, qB, b.w, COUNT ? ((mask >> (g0 + jj)) & 1u) : 1u);
+                    const f2 AL = f2_pack(alA, alB);
+                    const f2 T2 = f2_pack(TA, TB);
+                    float TnA, TnB, wA, wB;
+                    f2_split(f2_mul(T2, f2_rsub(AL, 1.0f)), TnA, TnB);                 // T (1 - alpha)
+                    f2_split(f2_mul(AL, T2), wA, wB);                                   // alpha T
                     if (COUNT) {
+                        const bool conA = passA && !(TnA < K_TMIN), conB = passB && !(TnB < K_TMIN);
                         cnt += (conA ? 1u : 0u) + (conB ? 1u : 0u);
                         tests += ((sqA && TA >= K_TMIN) ? 1u : 0u) + ((sqB && TB >= K_TMIN) ? 1u : 0u);
                     }
-                    eA[jj] = conA ? wA : 0.f;
-                    eB[jj] = conB ? wB : 0.f;
-                    TA = passA ? TnA : TA;  // pass && !con: the pixel ends (T < 1e-4)
-                    TB = passB ? TnB : TB;
+                    eA[jj] = !(TnA < K_TMIN) ? wA : 0.f;  // (w = 0 unless the fragment passes)
+                    eB[jj] = !(TnB < K_TMIN) ? wB : 0.f;
+                    TA = TnA;
+                    TB = TnB;
                 }
                 if (COUNT) wevals += 2 * RG;
                 // ---- reduce the group's weights per (slot, record) into the shared sums
