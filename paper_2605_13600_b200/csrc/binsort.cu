@@ -91,6 +91,9 @@ __device__ __forceinline__ void bs_walk(uint32_t k, uint32_t kend, uint32_t q0, 
     while (q < q1) {
         uint2 rc = make_uint2(0u, 1u);
         if (inc > exc && inc != 0xFFFFFFFFu) rc = __ldg(rect + e);
+        // m / w by multiply-high with ceil(2^32 / w), once per element (exact: m, w <= 12288)
+        const uint32_t wl = (rc.y & 0xFFFFu) - (rc.x & 0xFFFFu);
+        const uint32_t mg = wl > 1u ? 0xFFFFFFFFu / wl + 1u : 0u;
         uint32_t n_inc, n_exc, n_e;
         load(k + 32, n_inc, n_exc, n_e);
         const uint32_t last = __shfl_sync(FULL, inc, 31);  // entries of these 32 elements end here
@@ -107,12 +110,13 @@ __device__ __forceinline__ void bs_walk(uint32_t k, uint32_t kend, uint32_t q0, 
             const uint32_t ex = __shfl_sync(FULL, exc, l);
             const uint32_t rx = __shfl_sync(FULL, rc.x, l), ry = __shfl_sync(FULL, rc.y, l);
             const uint32_t el = __shfl_sync(FULL, e, l);
+            const uint32_t ml = __shfl_sync(FULL, mg, l);
             const bool valid = qq < qe;
             uint32_t b = 0xFFFFFFFFu;
             if (valid) {
                 const uint32_t m = qq - ex;
                 const uint32_t bx0 = rx & 0xFFFFu, by0 = rx >> 16, w = (ry & 0xFFFFu) - bx0;
-                const uint32_t r = m / w;
+                const uint32_t r = w == 1u ? m : __umulhi(m, ml);
                 b = (by0 + r) * (uint32_t)bins_x + bx0 + (m - r * w);
             }
             f(valid, qq, b, el);

@@ -234,10 +234,11 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
 // compactions over the batch indices (below), so index order is kept.
 
 // Summed-area table of the live tiles of each view: sat[v][(ty+1)*(tx_n+1) + tx+1] = number of
-// live tiles in [0, tx] x [0, ty].  One block per view; rows then columns, in shared memory.
+// live tiles in [0, tx] x [0, ty] (< 2^16: at most MAX_SAT_ENTRIES tiles).  One block per view;
+// rows then columns, in shared memory.
 
 __global__ void __launch_bounds__(1024) live_sat_kernel(const uint8_t* __restrict__ tile_live, int tiles_x,
-                                                        int tiles_y, uint32_t* __restrict__ sat) {
+                                                        int tiles_y, uint16_t* __restrict__ sat) {
     __shared__ uint32_t S[MAX_SAT_ENTRIES];
     const int v = blockIdx.x;
     const int W1 = tiles_x + 1, H1 = tiles_y + 1;
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(1024) live_sat_kernel(const uint8_t* __restric
     for (int x = threadIdx.x; x < W1; x += blockDim.x)
         for (int y = 1; y < H1; y++) S[y * W1 + x] += S[(y - 1) * W1 + x];
     __syncthreads();
-    for (int k = threadIdx.x; k < W1 * H1; k += blockDim.x) sat[(int64_t)v * W1 * H1 + k] = S[k];
+    for (int k = threadIdx.x; k < W1 * H1; k += blockDim.x) sat[(int64_t)v * W1 * H1 + k] = (uint16_t)S[k];
 }
 
 // ------------------------------------------------------------------ stable compaction
@@ -268,8 +269,8 @@ constexpr int SEL_TILE = 256 * SEL_ITEMS;
 
 struct NearSel {
     static constexpr bool kStageSat = false;
-    const uint32_t* ssat = nullptr;
-    const uint32_t* sat = nullptr;
+    const uint16_t* ssat = nullptr;
+    const uint16_t* sat = nullptr;
     int tiles_x = 0, tiles_y = 0;
     const uint32_t* code;
     const uint32_t* thr;
@@ -287,7 +288,7 @@ struct FarSel {
     int64_t G;
     uint32_t none;
     const uint32_t* trect;   // packed boxes from the depth pass, or NULL: recompute
-    const uint32_t* sat;     // live-tile summed-area tables
+    const uint16_t* sat;     // live-tile summed-area tables
     int tiles_x, tiles_y;
     PackedGaussians pg;
     const CamBatch* cams;    // device copy (recompute path)
@@ -317,11 +318,12 @@ struct FarSel {
         }
         if (x0 > x1 || y0 > y1) return false;
         const int W1 = tiles_x + 1;
-        const uint32_t* S = ssat;  // the view's table, staged in shared memory by the kernel
-        const uint32_t n = S[(y1 + 1) * W1 + x1 + 1] - S[y0 * W1 + x1 + 1] - S[(y1 + 1) * W1 + x0] + S[y0 * W1 + x0];
+        const uint16_t* S = ssat;  // the view's table, staged in shared memory by the kernel
+        const int n = (int)S[(y1 + 1) * W1 + x1 + 1] - (int)S[y0 * W1 + x1 + 1] - (int)S[(y1 + 1) * W1 + x0] +
+                      (int)S[y0 * W1 + x0];
         return n > 0;
     }
-    const uint32_t* ssat = nullptr;
+    const uint16_t* ssat = nullptr;
     static constexpr bool kStageSat = true;
 };
 
@@ -331,11 +333,11 @@ template <class Pred>
 __global__ void __launch_bounds__(256) sel_count_kernel(Pred pred, int64_t G, int tiles_per_view,
                                                         uint32_t* __restrict__ counts, uint32_t* __restrict__ bits) {
     __shared__ uint32_t ws[2][8];
-    extern __shared__ uint32_t sat_sh[];  // the far predicate's live-tile table of this view
+    extern __shared__ uint16_t sat_sh[];  // the far predicate's live-tile table of this view
     const int view = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (Pred::kStageSat) {
         const int n = (pred.tiles_x + 1) * (pred.tiles_y + 1);
-        const uint32_t* S = pred.sat + (int64_t)view * n;
+        const uint16_t* S = pred.sat + (int64_t)view * n;
         for (int k = threadIdx.x; k < n; k += blockDim.x) sat_sh[k] = S[k];
         pred.ssat = sat_sh;
         __syncthreads();
@@ -417,10 +419,19 @@ static void compact(const Pred& pred, int64_t G, int nviews, uint32_t* counts, u
     const dim3 grid(grid_for(G, SEL_TILE), (unsigned)nviews);
     const int64_t tiles = (int64_t)grid.x * grid.y;
     uint32_t* bits = counts + tiles;
-    const size_t smem = Pred::kStageSat ? sizeof(uint32_t) * (pred.tiles_x + 1) * (pred.tiles_y + 1) : 0;
+    const size_t smem = Pred::kStageSat ? sizeof(uint16_t) * (pred.tiles_x + 1) * (pred.tiles_y + 1) : 0;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(sel_count_kernel<Pred>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const dim3 cgrid(Pred::kStageSat ? std::min<unsigned>(grid.x, 256u) : grid.x, (unsigned)nviews);
+    // (the far predicate: one resident wave of blocks, each staging its view's table once)
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const unsigned per_view = (unsigned)std::max(1, (sms * 8) / std::max(1, nviews));
+    const dim3 cgrid(Pred::kStageSat ? std::min<unsigned>(grid.x, per_view) : grid.x, (unsigned)nviews);
     sel_count_kernel<Pred><<<cgrid, 256, smem, s>>>(pred, G, (int)grid.x, counts, bits);
     sel_scan_kernel<<<1, 1024, 0, s>>>(counts, (int)tiles, nsel);
     sel_scatter_kernel<<<grid, 256, 0, s>>>(G, counts, bits, sel);
@@ -597,8 +608,9 @@ __global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const
 
 // ------------------------------------------------------------------ Top-K (Eq. 6)
 // One thread per Gaussian row.  The KMAX best (value, atom) pairs live in registers,
-// ordered (value desc, atom asc); a new value bubbles in only if strictly larger than the
-// current KMAX-th, so equal values keep the lower atom (atoms are scanned ascending).
+// ordered (value desc, atom asc); a new value enters only if strictly larger than the current
+// KMAX-th and is shift-inserted after every equal value (atoms are scanned ascending), so ties
+// keep the lower atom.
 // Only positive values enter (registers start at 0).  Z_i cancels in the L1
 // renormalisation, so selection runs on the raw sums.
 // Optional by-product: the entropy of the
@@ -610,17 +622,41 @@ __global__ void ingest_codes_kernel(const uint32_t* __restrict__ atoms_in, const
 // order 0..P-1 for the fused cross-rank path (peers.n > 1) -- into padded shared rows (stride
 // L + 4 floats: a warp's LDS.128 of one column hits 8 distinct 16-B bank groups per wavefront),
 // then each thread runs the register insertion network on its own row.
+// Shift-insert of atom a (value v) into the list of the KMAX best so far, ordered (value desc,
+// atom asc).  Atoms arrive in ascending order, so v goes after every equal value (strict >):
+// the entries from its position on shift down by one and the last drops out.  (Comparing the
+// displaced entries again instead, as a bubble would, can drop an earlier atom of a tied value.)
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(float (&bv)[KMAX], uint32_t (&ba)[KMAX], float v, uint32_t a) {
+    float nv[KMAX];
+    uint32_t na[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) {
+        const bool here = v > bv[s];                    // v goes at or above slot s
+        const bool above = s > 0 && v > bv[s - 1];      // ... strictly above: slot s takes s - 1
+        nv[s] = above ? bv[s - 1] : (here ? v : bv[s]);
+        na[s] = above ? ba[s - 1] : (here ? a : ba[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < KMAX; s++) {
+        bv[s] = nv[s];
+        ba[s] = na[s];
+    }
+}
+
 #ifndef SCOUP_TOPK_ROWS
 #define SCOUP_TOPK_ROWS 128
 #endif
 constexpr int TOPK_ROWS = SCOUP_TOPK_ROWS;
 
-template <int KMAX>
+// LC: L / 4 at compile time (the common L = 64: constant row offsets and bit positions), or 0
+template <int KMAX, int LC>
 __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, int64_t rows, int64_t valid_rows, int L,
                                                               int K, uint32_t* __restrict__ atoms,
                                                               float* __restrict__ coefs, float* __restrict__ entropy) {
     extern __shared__ __align__(16) float tile[];
-    const int LP = L + 4, L4 = L >> 2;
+    if (LC) L = 4 * LC;
+    const int L4 = LC ? LC : (L >> 2), LP = L + 4;
     const int R = blockDim.x;  // rows per tile (one per thread)
     const int64_t r0 = (int64_t)blockIdx.x * R;
     const int64_t left = valid_rows - r0;
@@ -674,10 +710,11 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
     for (int s = 0; s < KMAX; s++) { bv[s] = 0.f; ba[s] = NONE; }
     if (t < nr) {
         const float4* row = reinterpret_cast<const float4*>(tile + t * LP);
-        for (int c4 = 0; c4 < L4; c4++) {
-            const float4 v4 = row[c4];
-            float vals[4] = {v4.x, v4.y, v4.z, v4.w};
-            if (entropy) {
+        const float* rowf = tile + t * LP;
+        if (entropy) {
+            for (int c4 = 0; c4 < L4; c4++) {
+                const float4 v4 = row[c4];
+                const float vals[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                 for (int u = 0; u < 4; u++)
                     if (vals[u] > 0.f) {
@@ -685,22 +722,53 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
                         hw += vals[u] * logf(vals[u]);
                     }
             }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                float v = vals[u];
-                if (v > bv[KMAX - 1]) {
-                    uint32_t a = (uint32_t)(c4 * 4 + u);
-#pragma unroll
-                    for (int s = 0; s < KMAX; s++) {
-                        bool sw = v > bv[s];
-                        float tv = sw ? bv[s] : v;
-                        uint32_t ta = sw ? ba[s] : a;
-                        bv[s] = sw ? v : bv[s];
-                        ba[s] = sw ? a : ba[s];
-                        v = tv;
-                        a = ta;
+        }
+        // Candidate bound: the maxima of K disjoint groups of atoms are K distinct elements, so at
+        // least K values are >= their minimum tau and no value below tau is in the Top-K.  Only
+        // the positive values >= tau (typically ~L/4 of a dense row) go through the insertion
+        // network -- in atom order, so ties keep the lower atom (strict >): the same selection and
+        // order as inserting every value.
+        float tau = 0.f;
+        if (L >= K) {
+            const int gs = L / K;
+            tau = __int_as_float(0x7f800000);
+            if ((gs & 3) == 0) {  // float4 groups (conflict-free LDS.128 on the padded rows)
+                const int g4 = gs >> 2;
+                for (int g = 0; g < K; g++) {
+                    const int c1 = g == K - 1 ? L4 : (g + 1) * g4;
+                    float m = 0.f;
+                    for (int c4 = g * g4; c4 < c1; c4++) {
+                        const float4 v4 = row[c4];
+                        m = fmaxf(m, fmaxf(fmaxf(v4.x, v4.y), fmaxf(v4.z, v4.w)));
                     }
+                    tau = fminf(tau, m);
                 }
+            } else {
+                for (int g = 0; g < K; g++) {
+                    const int a0 = g * gs, a1 = g == K - 1 ? L : a0 + gs;
+                    float m = rowf[a0];
+                    for (int a = a0 + 1; a < a1; a++) m = fmaxf(m, rowf[a]);
+                    tau = fminf(tau, m);
+                }
+            }
+        }
+        for (int c0 = 0; c0 < L4; c0 += 16) {  // chunks of 64 atoms: a candidate bit mask each
+            unsigned long long cm = 0ull;
+            const int c1 = min(L4, c0 + 16);
+            for (int c4 = c0; c4 < c1; c4++) {
+                const float4 v4 = row[c4];
+                const int sh = 4 * (c4 - c0);
+                cm |= (unsigned long long)((v4.x > 0.f && v4.x >= tau) ? 1u : 0u) << sh;
+                cm |= (unsigned long long)((v4.y > 0.f && v4.y >= tau) ? 2u : 0u) << sh;
+                cm |= (unsigned long long)((v4.z > 0.f && v4.z >= tau) ? 4u : 0u) << sh;
+                cm |= (unsigned long long)((v4.w > 0.f && v4.w >= tau) ? 8u : 0u) << sh;
+            }
+            while (cm) {
+                const int bit = __ffsll((long long)cm) - 1;
+                cm &= cm - 1ull;
+                const uint32_t a = (uint32_t)(4 * c0 + bit);
+                const float v = rowf[a];
+                if (v > bv[KMAX - 1]) topk_insert<KMAX>(bv, ba, v, a);
             }
         }
     }
@@ -764,19 +832,7 @@ __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restric
                 hs += v;
                 hw += v * logf(v);
             }
-            if (v > bv[KMAX - 1]) {
-                uint32_t a = (uint32_t)c;
-#pragma unroll
-                for (int s = 0; s < KMAX; s++) {
-                    bool sw = v > bv[s];
-                    float tv = sw ? bv[s] : v;
-                    uint32_t ta = sw ? ba[s] : a;
-                    bv[s] = sw ? v : bv[s];
-                    ba[s] = sw ? a : ba[s];
-                    v = tv;
-                    a = ta;
-                }
-            }
+            if (v > bv[KMAX - 1]) topk_insert<KMAX>(bv, ba, v, (uint32_t)c);
         }
     }
     float sum = 0.f;
@@ -815,9 +871,10 @@ void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_b
 void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
                         const Binning& bn, uint32_t* counts, cudaStream_t s) {
     if (G <= 0 || nviews <= 0) return;
-    live_sat_kernel<<<nviews, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, vb.live_sat);
+    uint16_t* sat = reinterpret_cast<uint16_t*>(vb.live_sat);
+    live_sat_kernel<<<nviews, 1024, 0, s>>>(vb.tile_live, bn.tiles_x, bn.tiles_y, sat);
     const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
-    const FarSel pred{vb.code, vb.thr, G, (1u << key_bits) - 1u, packed ? vb.trect : nullptr, vb.live_sat,
+    const FarSel pred{vb.code, vb.thr, G, (1u << key_bits) - 1u, packed ? vb.trect : nullptr, sat,
                       bn.tiles_x, bn.tiles_y, pg, vb.cams};
     compact(pred, G, nviews, counts, vb.sel, vb.nsel, s);
 }
@@ -868,25 +925,32 @@ void launch_ingest_codes(const uint32_t* atoms_in, const float* coefs_in, int64_
 // peers' memory (CUDA IPC mappings over NVLink / NVSwitch), in rank order 0..P-1 -- and Eq. 6
 // runs on the sums (topk_tile_kernel with P partials).  This replaces reduce-scatter + Top-K: no
 // reduced shard is written and re-read.
-template <int KMAX>
+template <int KMAX, int LC>
 static void topk_tile_launch(PeerRows peers, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
                              float* coefs, float* entropy, cudaStream_t s) {
     const int R = L <= 256 ? TOPK_ROWS : 32;  // rows per CTA: <= 133 KB of staged rows (L <= SCOUP_MAX_L)
     const size_t smem = (size_t)R * (L + 4) * sizeof(float);
     static int smem_set = 0;  // opt-in above 48 KB, once per instantiation and size
     if (smem > 48 * 1024 && smem_set < (int)smem) {
-        cudaFuncSetAttribute(topk_tile_kernel<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(topk_tile_kernel<KMAX, LC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         smem_set = (int)smem;
     }
-    topk_tile_kernel<KMAX><<<grid_for(rows, R), R, smem, s>>>(peers, rows, valid_rows, L, K, atoms, coefs, entropy);
+    topk_tile_kernel<KMAX, LC><<<grid_for(rows, R), R, smem, s>>>(peers, rows, valid_rows, L, K, atoms, coefs, entropy);
+}
+
+template <int KMAX>
+static void topk_tile_l(PeerRows peers, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
+                        float* coefs, float* entropy, cudaStream_t s) {
+    if (L == 64) topk_tile_launch<KMAX, 16>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else topk_tile_launch<KMAX, 0>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
 }
 
 static void topk_tile(const PeerRows& peers, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms,
                       float* coefs, float* entropy, cudaStream_t s) {
-    if (K <= 4) topk_tile_launch<4>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else if (K <= 8) topk_tile_launch<8>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else if (K <= 16) topk_tile_launch<16>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
-    else topk_tile_launch<32>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    if (K <= 4) topk_tile_l<4>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 8) topk_tile_l<8>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else if (K <= 16) topk_tile_l<16>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
+    else topk_tile_l<32>(peers, rows, valid_rows, L, K, atoms, coefs, entropy, s);
 }
 
 void launch_topk_peers(const PeerRows& peers, int64_t first_row, int64_t rows, int64_t valid_rows, int L, int K,

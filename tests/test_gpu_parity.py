@@ -727,3 +727,38 @@ def test_render_code_lengths(dev, tiny_scene, K):
     ref = oracle_render(g, scene.cameras[:2], atoms, coefs, cfg.L)
     assert np.abs(ref).max() > 0.05
     assert np.all(np.abs(Wh - ref) <= 1e-6 + 1e-5 * np.abs(ref))
+
+
+@pytest.mark.parametrize("L,K,density,levels", [(64, 8, 1.0, 6), (64, 8, 0.3, 0), (64, 4, 1.0, 3), (10, 4, 0.7, 4),
+                                                (100, 16, 1.0, 5), (64, 1, 1.0, 2), (8, 8, 1.0, 3)])
+def test_topk_kernel_exact_on_dense_rows_with_ties(dev, L, K, density, levels):
+    """Eq. 6 selection on finalize_topk's own rows: dense and sparse random rows, some
+    drawn from a few discrete levels so that exact ties at the K-th value are common, plus all-zero,
+    single-positive and all-equal rows and negative entries.  The atoms must equal oracle.topk's
+    (value desc, atom asc, positive only) EXACTLY -- the candidate bound (minimum of K group
+    maxima) may not change the tie rule -- and the coefficients its fp64 L1 renormalisation to
+    fp32 rounding."""
+    from paper_2605_13600_b200.uplift import SparseUplift
+    rng = np.random.default_rng([L, K, levels])
+    G = 20_000
+    if levels:
+        W = rng.integers(0, levels, size=(G, L)).astype(np.float32) * np.float32(0.25)
+    else:
+        W = rng.random((G, L), dtype=np.float32)
+    W = np.where(rng.random((G, L)) < density, W, 0.0).astype(np.float32)
+    W[0] = 0.0
+    W[1] = 0.0
+    W[1, L - 1] = 1.0
+    W[2] = 0.5
+    W[3] = -rng.random(L).astype(np.float32)
+    W[4, : L // 2] = -1.0
+    g = synth.Gaussians(np.zeros((G, 3), np.float32), np.full((G, 3), 0.1, np.float32),
+                        np.tile(np.array([[1, 0, 0, 0]], np.float32), (G, 1)), np.full((G,), 0.5, np.float32))
+    with SparseUplift(g, L, K, rows_padded=G) as up:
+        a, c = up.finalize(0, G, W_rows=torch.from_numpy(W).to(dev))
+        torch.cuda.synchronize()
+        a = a.cpu().numpy().view(np.uint32)
+        c = c.cpu().numpy().astype(np.float64)
+    ao, co = oracle.topk(W, K)
+    assert np.array_equal(a, ao), np.argwhere(np.any(a != ao, axis=1))[:5].ravel()
+    assert np.all(np.abs(c - co) <= 1e-6 * np.abs(co) + 1e-7)
