@@ -428,7 +428,7 @@ struct CallArgs {
     float* r_out = nullptr;
 };
 
-// Depth pass of a batch: codes, per-view histogram (-> host), camera copy for the predicates.
+// Split histogram of a batch (sampled depth codes, per view -> host), camera copy for the passes.
 void step_depth(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     ViewBuffers& b = c.vb;
     Ctx::EvSet* es = ev_begin(h, c);
@@ -439,7 +439,7 @@ void step_depth(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     *c.h_cams = c.cams;
     CK(cudaMemcpyAsync(b.cams, c.h_cams, sizeof(CamBatch), cudaMemcpyHostToDevice, c.s));
     CK(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * NHIST * c.nv, c.s));
-    launch_depth_pass(h->pg, h->G, c.cams, c.key_bits, b.code, b.hist, h->d_stats + 3, latch_of(h), a.bn, b.trect, c.s);
+    launch_depth_hist(h->pg, h->G, c.cams, c.key_bits, b.hist, c.s);
     CK(cudaMemcpyAsync(c.h_hist, b.hist, sizeof(uint32_t) * NHIST * c.nv, cudaMemcpyDeviceToHost, c.s));
     CK(cudaEventRecord(c.ev, c.s));
     h->kernel_launches += 1;
@@ -481,7 +481,6 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
 // boundary of the depth code), stable-compacted, then the chunk front.
 void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     CK(cudaEventSynchronize(c.ev));
-    (void)a;
     const uint32_t none = (1u << c.key_bits) - 1u;
     const int shift = c.key_bits > HIST_BITS ? c.key_bits - HIST_BITS : 0;
     c.far_any = false;
@@ -511,7 +510,9 @@ void step_near_front(scoup_uplift* h, Ctx& c, const CallArgs& a) {
     }
     ViewBuffers& b = c.vb;
     CK(cudaMemcpyAsync(b.thr, c.h_thr, sizeof(uint32_t) * c.nv, cudaMemcpyHostToDevice, c.s));
-    launch_select_near2(b, h->G, c.nv, c.key_bits, b.selcnt, c.s);
+    // the full depth pass: codes, reach boxes and the near chunk's compaction in one sweep
+    launch_depth_pass_near(h->pg, h->G, c.cams, c.key_bits, b.thr, b.code, h->d_stats + 3, latch_of(h), a.bn, b.trect,
+                           b.selcnt, b.sel, b.nsel, c.s);
     h->kernel_launches += 3;
     CK(cudaMemcpyAsync(c.h_nsel, b.nsel, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     CK(cudaEventRecord(c.ev, c.s));

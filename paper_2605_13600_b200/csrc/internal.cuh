@@ -24,7 +24,7 @@ constexpr int MAX_LEV = 4;               // semantic levels fused per raster pas
 constexpr int MAX_SAT_ENTRIES = 12288;   // (tiles_x + 1) * (tiles_y + 1): 1920x1080 needs 121 x 69
 constexpr int HIST_BITS = 10;            // depth-code histogram resolution (near/far split)
 constexpr int NHIST = 1 << HIST_BITS;
-constexpr int HIST_SAMPLE = 8;           // the depth histogram counts every 8th Gaussian
+constexpr int HIST_SAMPLE = 32;          // the depth histogram counts every 32nd Gaussian
 
 // DESIGN.md §3 constants (hex-exact fp32)
 #define K_NEAR 0x1.99999ap-3f
@@ -390,9 +390,11 @@ __device__ __forceinline__ f2 exp2_spec2(f2 y) {
 void launch_activate(const float* means, const float* scales, const float* rots, const float* opac,
                      int64_t G, PackedGaussians pg, ErrorLatch err, cudaStream_t s);
 void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s);
-void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* code,
-                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
-                       uint32_t* trect, cudaStream_t s);
+void launch_depth_hist(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* hist,
+                       cudaStream_t s);
+void launch_depth_pass_near(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, const uint32_t* thr,
+                            uint32_t* code, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
+                            uint32_t* trect, uint32_t* counts, uint32_t* sel, int* nsel, cudaStream_t s);
 // stable compactions into vb.sel / vb.nsel; temp storage grown through *tmp / *tmp_bytes
 void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
                        int key_bits, int64_t nsel, cudaStream_t s);
@@ -407,7 +409,6 @@ int select_tiles_per_view(int64_t G);
 // custom stable compactions (kernels.cu): near / far chunk selections into vb.sel, count into
 // vb.nsel; counts = scratch of select_counts_needed(G, nviews) tile counts
 size_t select_counts_needed(int64_t G, int nviews);
-void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, uint32_t* counts, cudaStream_t s);
 void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
                         const Binning& bn, uint32_t* counts, cudaStream_t s);
 void launch_ingest_dense(const float* in, int64_t n, float* out, ErrorLatch err, cudaStream_t s);

@@ -148,12 +148,10 @@ __device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const
     return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height;
 }
 
-// One thread per (view, Gaussian), grid.y = view.  Writes code[j] (j = v*G + i) and the per-view
-// histogram of the codes' top HIST_BITS bits (near/far split, DESIGN.md §5 a3).  Off-screen
-// Gaussians (conservative reach misses the image) are invisible.
-// Each block covers ITEMS_PER_THREAD * 256 consecutive Gaussians of one view, so that the
-// shared histogram and the visible count are flushed to global memory once per block.
-constexpr int ITEMS_PER_THREAD = 16;
+// Stable compactions over the batch indices (below) and the depth pass share one tiling: tiles of
+// SEL_TILE Gaussians per view, 8 warps each owning SEL_ITEMS rounds of 32 consecutive Gaussians.
+constexpr int SEL_ITEMS = 16;
+constexpr int SEL_TILE = 256 * SEL_ITEMS;
 
 // Packed reach box in 16x16 tiles for the far-chunk predicate (x0 | x1 << 8 | y0 << 16 | y1 << 24;
 // x0 > x1: no tile); images up to 255 tiles a side (wider ones recompute in far_flags).
@@ -169,63 +167,110 @@ __device__ __forceinline__ uint32_t tile_rect(float mx, float my, float rb, int 
     return (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
 }
 
-__global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
-                                                         int key_bits, uint32_t* __restrict__ code,
-                                                         uint32_t* __restrict__ hist, unsigned long long* visible_ctr,
-                                                         ErrorLatch err, int tiles_x, int tiles_y,
-                                                         uint32_t* __restrict__ trect) {
+// Depth code of Gaussian i in the view (V1, V2, the conservative on-screen test) and, when
+// visible, its packed reach box in 16x16 tiles.
+__device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const Camera& cam, uint32_t none,
+                                               int tiles_x, int tiles_y, bool want_rect, uint32_t& rect,
+                                               bool& beyond) {
+    uint32_t c = none;
+    rect = TRECT_EMPTY;
+    beyond = false;
+    float t[3];
+    camera_space(A, cam, t);
+    if (t[2] > K_NEAR && A.w >= K_AMIN) {
+        float mx, my, rb;
+        reach_fast(t, s2, cam, mx, my, rb);
+        if (box_on_image(mx, my, rb, cam)) {
+            c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
+            if (!(c < none)) {  // beyond the host's depth bound for the batch (cannot happen)
+                beyond = true;
+                c = none;
+            }
+            if (want_rect) rect = tile_rect(mx, my, rb, tiles_x, tiles_y);
+        }
+    }
+    return c;
+}
+
+// The split histogram (DESIGN.md §5 a3): the codes' top HIST_BITS bits of every HIST_SAMPLE-th
+// Gaussian per view (the split is a heuristic -- any threshold is exact -- and the near count
+// comes from the compaction).  One thread per sampled (view, Gaussian).
+__global__ void __launch_bounds__(256) depth_hist_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                         int key_bits, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[NHIST];
-    __shared__ uint32_t svis;
     for (int k = threadIdx.x; k < NHIST; k += blockDim.x) sh[k] = 0;
-    if (threadIdx.x == 0) svis = 0;
     __syncthreads();
     const int view = blockIdx.y;
-    const Camera cam = cams.cam[view];  // (a register copy: no per-use parameter loads)
+    const Camera cam = cams.cam[view];
     const uint32_t none = (1u << key_bits) - 1u;
     const int shift = key_bits > HIST_BITS ? key_bits - HIST_BITS : 0;
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS_PER_THREAD;
-    uint32_t nvis = 0;
-#pragma unroll 4
-    for (int it = 0; it < ITEMS_PER_THREAD; it++) {
-        const int64_t i = base + (int64_t)it * blockDim.x + threadIdx.x;
-        bool vis = false;
-        int bucket = -1;
-        if (i < G) {
-            const float4 A = pg.a[i];
-            uint32_t c = none, rect = TRECT_EMPTY;
-            float t[3];
-            camera_space(A, cam, t);
-            if (t[2] > K_NEAR && A.w >= K_AMIN) {
-                float mx, my, rb;
-                reach_fast(t, pg.s2[i], cam, mx, my, rb);
-                if (box_on_image(mx, my, rb, cam)) {
-                    c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
-                    vis = c < none;
-                    if (!vis) {  // beyond the host's depth bound for the batch (cannot happen)
-                        latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + i);
-                        c = none;
-                    }
-                    if (trect) rect = tile_rect(mx, my, rb, tiles_x, tiles_y);
-                }
-            }
-            code[(int64_t)view * G + i] = c;
-            if (trect) trect[(int64_t)view * G + i] = rect;
-            // the split histogram samples every HIST_SAMPLE-th Gaussian (the split is a
-            // heuristic: any threshold is exact; the near count comes from the compaction)
-            bucket = vis && (i & (HIST_SAMPLE - 1)) == 0 ? (int)(c >> shift) : -1;
-        }
-        // warp-aggregated histogram: one shared atomic per distinct bucket in the warp (the depth
-        // codes of a scene concentrate in few buckets: plain per-lane atomics contend)
-        const unsigned peers = __match_any_sync(0xffffffffu, bucket);
-        if (bucket >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bucket], (uint32_t)__popc(peers));
-        nvis += vis ? 1u : 0u;
+    const int64_t n = (G + HIST_SAMPLE - 1) / HIST_SAMPLE;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = k * HIST_SAMPLE;
+        uint32_t rect;
+        bool beyond;
+        const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, none, 0, 0, false, rect, beyond);
+        if (c != none) atomicAdd(&sh[c >> shift], 1u);
     }
-    nvis = __reduce_add_sync(0xffffffffu, nvis);
-    if ((threadIdx.x & 31) == 0 && nvis) atomicAdd(&svis, nvis);
     __syncthreads();
     for (int k = threadIdx.x; k < NHIST; k += blockDim.x)
         if (sh[k]) atomicAdd(&hist[view * NHIST + k], sh[k]);
-    if (threadIdx.x == 0 && svis) atomicAdd(visible_ctr, (unsigned long long)svis);
+}
+
+// One thread per (view, Gaussian), grid (tiles of SEL_TILE Gaussians, view): writes code[j]
+// (j = v*G + i) and the packed reach box, counts the visible Gaussians, and runs the count pass of
+// the near chunk's stable compaction in the same sweep (code < thr[v]: the predicate words and
+// tile counts sel_scan / sel_scatter take, laid out as sel_count_kernel's).  Off-screen Gaussians
+// (conservative reach misses the image) are invisible.
+__global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
+                                                         int key_bits, const uint32_t* __restrict__ thr,
+                                                         uint32_t* __restrict__ code,
+                                                         unsigned long long* visible_ctr, ErrorLatch err, int tiles_x,
+                                                         int tiles_y, uint32_t* __restrict__ trect,
+                                                         uint32_t* __restrict__ counts, uint32_t* __restrict__ bits) {
+    __shared__ uint32_t ws[8], wv[8];
+    const int view = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Camera cam = cams.cam[view];  // (a register copy: no per-use parameter loads)
+    const uint32_t none = (1u << key_bits) - 1u;
+    const uint32_t tv = thr[view];
+    const int64_t base = (int64_t)blockIdx.x * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
+    const int64_t tile = (int64_t)view * gridDim.x + blockIdx.x;
+    uint32_t n = 0, nvis = 0, word = 0;
+#pragma unroll 4
+    for (int it = 0; it < SEL_ITEMS; it++) {
+        const int64_t i = base + it * 32;
+        bool near = false;
+        if (i < G) {
+            uint32_t rect;
+            bool beyond;
+            const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, none, tiles_x, tiles_y, trect != nullptr, rect, beyond);
+            if (beyond) latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + i);
+            code[(int64_t)view * G + i] = c;
+            if (trect) trect[(int64_t)view * G + i] = rect;
+            nvis += c != none ? 1u : 0u;
+            near = c < tv && c != none;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, near);
+        n += __popc(b);
+        if (lane == it) word = b;  // the warp's 16 predicate words, one per lane, for the scatter
+    }
+    if (lane < SEL_ITEMS) bits[(tile * 8 + warp) * SEL_ITEMS + lane] = word;
+    nvis = __reduce_add_sync(0xffffffffu, nvis);
+    if (lane == 0) {
+        ws[warp] = n;
+        wv[warp] = nvis;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0, vis = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+            tot += ws[w];
+            vis += wv[w];
+        }
+        counts[tile] = tot;
+        if (vis) atomicAdd(visible_ctr, (unsigned long long)vis);
+    }
 }
 
 // ------------------------------------------------------------------ chunk selection
@@ -264,23 +309,6 @@ __global__ void __launch_bounds__(1024) live_sat_kernel(const uint8_t* __restric
 // warp owns 512 consecutive elements of its tile (16 rounds of 32), so ranks are ballot prefix
 // sums in order.  Predicates: the near chunk (code below the view's split), the far chunk (code
 // at or beyond the split and the conservative reach box covering a live tile).
-constexpr int SEL_ITEMS = 16;
-constexpr int SEL_TILE = 256 * SEL_ITEMS;
-
-struct NearSel {
-    static constexpr bool kStageSat = false;
-    const uint16_t* ssat = nullptr;
-    const uint16_t* sat = nullptr;
-    int tiles_x = 0, tiles_y = 0;
-    const uint32_t* code;
-    const uint32_t* thr;
-    int64_t G;
-    uint32_t none;
-    __device__ __forceinline__ uint2 load(int view, int64_t i) const {
-        return make_uint2(code[(int64_t)view * G + i], 0u);
-    }
-    __device__ __forceinline__ bool test(int view, int64_t i, uint2 v) const { return v.x < thr[view] && v.x != none; }
-};
 
 struct FarSel {
     const uint32_t* code;
@@ -858,16 +886,6 @@ size_t select_counts_needed(int64_t G, int nviews) {
     return (size_t)grid_for(G, SEL_TILE) * (size_t)nviews * (1 + 8 * SEL_ITEMS);
 }
 
-void launch_select_near2(const ViewBuffers& vb, int64_t G, int nviews, int key_bits, uint32_t* counts, cudaStream_t s) {
-    if (G <= 0 || nviews <= 0) return;
-    NearSel pred;
-    pred.code = vb.code;
-    pred.thr = vb.thr;
-    pred.G = G;
-    pred.none = (1u << key_bits) - 1u;
-    compact(pred, G, nviews, counts, vb.sel, vb.nsel, s);
-}
-
 void launch_select_far2(const ViewBuffers& vb, PackedGaussians pg, int64_t G, int nviews, int key_bits,
                         const Binning& bn, uint32_t* counts, cudaStream_t s) {
     if (G <= 0 || nviews <= 0) return;
@@ -891,14 +909,26 @@ void launch_bounds(PackedGaussians pg, int64_t G, int* bbox, cudaStream_t s) {
     bounds_kernel<<<(unsigned)blocks, 256, 0, s>>>(pg, G, bbox);
 }
 
-void launch_depth_pass(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* code,
-                       uint32_t* hist, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
-                       uint32_t* trect, cudaStream_t s) {
+void launch_depth_hist(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, uint32_t* hist,
+                       cudaStream_t s) {
     if (G <= 0 || cams.n <= 0) return;
-    dim3 grid(grid_for(G, 256 * ITEMS_PER_THREAD), (unsigned)cams.n);
+    const int64_t n = (G + HIST_SAMPLE - 1) / HIST_SAMPLE;
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)cams.n);
+    depth_hist_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, hist);
+}
+
+void launch_depth_pass_near(PackedGaussians pg, int64_t G, const CamBatch& cams, int key_bits, const uint32_t* thr,
+                            uint32_t* code, unsigned long long* visible_ctr, ErrorLatch err, const Binning& bn,
+                            uint32_t* trect, uint32_t* counts, uint32_t* sel, int* nsel, cudaStream_t s) {
+    if (G <= 0 || cams.n <= 0) return;
+    const dim3 grid(grid_for(G, SEL_TILE), (unsigned)cams.n);
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    uint32_t* bits = counts + tiles;
     const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
-    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, code, hist, visible_ctr, err, bn.tiles_x, bn.tiles_y,
-                                           packed ? trect : nullptr);
+    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, thr, code, visible_ctr, err, bn.tiles_x, bn.tiles_y,
+                                           packed ? trect : nullptr, counts, bits);
+    sel_scan_kernel<<<1, 1024, 0, s>>>(counts, (int)tiles, nsel);
+    sel_scatter_kernel<<<grid, 256, 0, s>>>(G, counts, bits, sel);
 }
 
 void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
