@@ -40,7 +40,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BS_WARPS_MAX = 8;
 // a view has at most MAX_SAT_ENTRIES 16x16 tiles and bins are >= 1 tile: one warp's row fits
-static_assert(MAX_SAT_ENTRIES * sizeof(uint32_t) <= 200 * 1024, "bin row in shared memory");
+static_assert(MAX_SAT_ENTRIES * 5 <= 200 * 1024, "bin row (+ lane tags) in shared memory");
 
 // The segment of warp `seg`: its view and entry range [q0, q1) (chunk-flattened positions).
 __device__ __forceinline__ bool bs_segment(const BsInfo* info, int nv, uint32_t seg, int& v, uint32_t& q0,
@@ -269,6 +269,7 @@ __global__ void bs_scatter_kernel(const BsInfo* __restrict__ info, int nv, int n
     uint32_t q0, q1;
     if (!bs_segment(info, nv, seg, v, q0, q1)) return;
     uint32_t* row = bs_rows + (size_t)warp * nb;
+    uint8_t* tag = reinterpret_cast<uint8_t*>(bs_rows + (size_t)(blockDim.x >> 5) * nb) + (size_t)warp * nb;
     const uint32_t* pre = cnt + (size_t)seg * nb;
     const uint2* R = ranges + (size_t)v * nb;
     for (int b = lane; b < nb; b += 32) row[b] = R[b].x + pre[b];
@@ -289,12 +290,25 @@ __global__ void bs_scatter_kernel(const BsInfo* __restrict__ info, int nv, int n
             // bin's earlier lanes are earlier elements: rank = earlier peers
             const uint32_t b = bb[u];
             const bool valid = b != 0xFFFFFFFFu;
-            const unsigned peers = __match_any_sync(FULL, b);
-            const uint32_t pos = valid ? row[b] + (uint32_t)__popc(peers & lt) : 0u;
+            // common case: the step's bins are distinct (its entries are mostly a few elements'
+            // rectangles) -- detected by a lane-id tag per bin, no warp match needed
+            if (valid) tag[b] = (uint8_t)lane;
             __syncwarp();
-            if (valid) {
-                eval[pos] = ee[u];
-                if (lane == 31 - __clz(peers)) row[b] = pos + 1u;  // the bin's last entry of this step
+            const bool own = !valid || tag[b] == (uint8_t)lane;
+            if (__all_sync(FULL, own)) {
+                if (valid) {
+                    const uint32_t pos = row[b];
+                    eval[pos] = ee[u];
+                    row[b] = pos + 1u;
+                }
+            } else {
+                const unsigned peers = __match_any_sync(FULL, b);
+                const uint32_t pos = valid ? row[b] + (uint32_t)__popc(peers & lt) : 0u;
+                __syncwarp();
+                if (valid) {
+                    eval[pos] = ee[u];
+                    if (lane == 31 - __clz(peers)) row[b] = pos + 1u;  // the bin's last entry of this step
+                }
             }
             __syncwarp();
         }
@@ -327,14 +341,22 @@ void launch_binsort(const uint32_t* sel_offsets, int tiles_per_view, const uint3
     static size_t smem_set = 48 * 1024;
     if (smem > smem_set) {
         cudaFuncSetAttribute(bs_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(bs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         smem_set = smem;
     }
     const unsigned grid = (unsigned)((binsort_segments_max(entries, nv) + wpc - 1) / wpc);
     bs_count_kernel<<<grid, 32 * wpc, smem, s>>>(info, nv, offs, sval_sorted, rect, bins_x, nb, cnt, ebin, eel);
     bs_colscan_kernel<<<dim3((unsigned)((nb + 31) / 32), (unsigned)nv), 256, 0, s>>>(info, nb, cnt, ranges);
     bs_ranges_kernel<<<nv, 1024, 0, s>>>(info, nb, ranges);
-    bs_scatter_kernel<<<grid, 32 * wpc, smem, s>>>(info, nv, nb, cnt, ranges, ebin, eel, eval);
+    // (the scatter's rows plus a byte of lane tag per bin)
+    const int wps = std::max(1, std::min(BS_WARPS_MAX, (int)((96 * 1024) / ((size_t)nb * 5))));
+    const size_t smem_s = (size_t)wps * nb * 5;
+    static size_t smem_set_s = 48 * 1024;
+    if (smem_s > smem_set_s) {
+        cudaFuncSetAttribute(bs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+        smem_set_s = smem_s;
+    }
+    const unsigned grid_s = (unsigned)((binsort_segments_max(entries, nv) + wps - 1) / wps);
+    bs_scatter_kernel<<<grid_s, 32 * wps, smem_s, s>>>(info, nv, nb, cnt, ranges, ebin, eel, eval);
 }
 
 }  // namespace scoup

@@ -147,6 +147,9 @@ __device__ __forceinline__ void reach_fast(const float t[3], float s2max, const 
 __device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const Camera& cam) {
     return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height;
 }
+__device__ __forceinline__ bool box_on_image(float mx, float my, float rb, float Wf, float Hf) {
+    return mx + rb >= 0.f && mx - rb <= Wf && my + rb >= 0.f && my - rb <= Hf;
+}
 
 // Stable compactions over the batch indices (below) and the depth pass share one tiling: tiles of
 // SEL_TILE Gaussians per view, 8 warps each owning SEL_ITEMS rounds of 32 consecutive Gaussians.
@@ -169,9 +172,9 @@ __device__ __forceinline__ uint32_t tile_rect(float mx, float my, float rb, int 
 
 // Depth code of Gaussian i in the view (V1, V2, the conservative on-screen test) and, when
 // visible, its packed reach box in 16x16 tiles.
-__device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const Camera& cam, uint32_t none,
-                                               int tiles_x, int tiles_y, bool want_rect, uint32_t& rect,
-                                               bool& beyond) {
+__device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const Camera& cam, float Wf, float Hf,
+                                               uint32_t none, int tiles_x, int tiles_y, bool want_rect,
+                                               uint32_t& rect, bool& beyond) {
     uint32_t c = none;
     rect = TRECT_EMPTY;
     beyond = false;
@@ -180,7 +183,7 @@ __device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const 
     if (t[2] > K_NEAR && A.w >= K_AMIN) {
         float mx, my, rb;
         reach_fast(t, s2, cam, mx, my, rb);
-        if (box_on_image(mx, my, rb, cam)) {
+        if (box_on_image(mx, my, rb, Wf, Hf)) {
             c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
             if (!(c < none)) {  // beyond the host's depth bound for the batch (cannot happen)
                 beyond = true;
@@ -209,7 +212,8 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(PackedGaussians pg, int
         const int64_t i = k * HIST_SAMPLE;
         uint32_t rect;
         bool beyond;
-        const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, none, 0, 0, false, rect, beyond);
+        const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, (float)cam.width, (float)cam.height, none, 0, 0, false,
+                                      rect, beyond);
         if (c != none) atomicAdd(&sh[c >> shift], 1u);
     }
     __syncthreads();
@@ -233,20 +237,27 @@ __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int
     const Camera cam = cams.cam[view];  // (a register copy: no per-use parameter loads)
     const uint32_t none = (1u << key_bits) - 1u;
     const uint32_t tv = thr[view];
+    const float Wf = (float)cam.width, Hf = (float)cam.height;
     const int64_t base = (int64_t)blockIdx.x * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
     const int64_t tile = (int64_t)view * gridDim.x + blockIdx.x;
+    // this thread's Gaussians i = base + 32 it and their (view, Gaussian) slots, as offsets
+    const float4* pa = pg.a + base;
+    const float* ps = pg.s2 + base;
+    uint32_t* pc = code + (int64_t)view * G + base;
+    uint32_t* pr = trect ? trect + (int64_t)view * G + base : nullptr;
+    const int nit = (int)max((int64_t)0, min((int64_t)SEL_ITEMS, (G - base + 31) / 32));  // items with i < G
     uint32_t n = 0, nvis = 0, word = 0;
-#pragma unroll 4
+#pragma unroll 8
     for (int it = 0; it < SEL_ITEMS; it++) {
-        const int64_t i = base + it * 32;
         bool near = false;
-        if (i < G) {
+        if (it < nit) {
             uint32_t rect;
             bool beyond;
-            const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, none, tiles_x, tiles_y, trect != nullptr, rect, beyond);
-            if (beyond) latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + i);
-            code[(int64_t)view * G + i] = c;
-            if (trect) trect[(int64_t)view * G + i] = rect;
+            const uint32_t c = depth_code(pa[32 * it], ps[32 * it], cam, Wf, Hf, none, tiles_x, tiles_y, pr != nullptr,
+                                          rect, beyond);
+            if (beyond) latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + base + 32 * it);
+            pc[32 * it] = c;
+            if (pr) pr[32 * it] = rect;
             nvis += c != none ? 1u : 0u;
             near = c < tv && c != none;
         }
