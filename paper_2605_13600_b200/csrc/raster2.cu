@@ -361,8 +361,13 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                         cnt += (conA ? 1u : 0u) + (conB ? 1u : 0u);
                         tests += ((sqA && TA >= K_TMIN) ? 1u : 0u) + ((sqB && TB >= K_TMIN) ? 1u : 0u);
                     }
-                    eA[jj] = !(TnA < K_TMIN) ? wA : 0.f;  // (w = 0 unless the fragment passes)
-                    eB[jj] = !(TnB < K_TMIN) ? wB : 0.f;
+                    // e = w where the pixel continues (!(Tn < 1e-4)), else 0 (w = 0 unless the
+                    // fragment passes): w times a 1.0 / 0.0 flag (PTX set: one ALU op per pixel
+                    // instead of a compare and a select; the product is exact)
+                    float gA, gB;
+                    asm("set.geu.f32.f32 %0, %1, %2;" : "=f"(gA) : "f"(TnA), "f"(K_TMIN));
+                    asm("set.geu.f32.f32 %0, %1, %2;" : "=f"(gB) : "f"(TnB), "f"(K_TMIN));
+                    f2_split(f2_mul(f2_pack(wA, wB), f2_pack(gA, gB)), eA[jj], eB[jj]);
                     TA = TnA;
                     TB = TnB;
                 }
