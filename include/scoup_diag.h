@@ -26,6 +26,13 @@ extern "C" {
 int scoup_diag_red_rate(int device, int64_t buffer_bytes, int scattered, int vec4, int64_t reds_per_launch,
                         int launches, double *adds_per_s, double *ms_per_launch);
 
+/* Entries per warp segment of the binning's stable counting sort (DESIGN.md §5 a3; process-wide):
+ * entries_per_segment > 0 forces that length (rounded up to a multiple of 32; tests use it to
+ * exercise the long segments large chunks get), 0 restores the adaptive choice (2048 entries, more
+ * for chunks so large that the [segment][bin] count matrix would dominate).  Returns 0, or 1 if
+ * entries_per_segment is negative or above 2^24. */
+int scoup_diag_set_binsort_segment(int entries_per_segment);
+
 /* Thread-local message of the last failing diag call ("" if none). */
 const char *scoup_diag_last_error(void);
 

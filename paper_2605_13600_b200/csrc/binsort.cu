@@ -6,7 +6,7 @@
 // covering the bin.  Instead of expanding (bin, element) entries and radix-sorting them by bin,
 // the lists are written straight to their final positions.  The chunk's entries, flattened in
 // element order (an element's bins row-major over its rectangle), are cut per view into
-// segments of BS_SEGE entries (equal work: the nearest Gaussians cover many bins):
+// segments of BS_SEGE entries or more (equal work: the nearest Gaussians cover many bins):
 //
 //   bs_gather   entry counts in sorted order (-> CUB inclusive scan: offs) and their u64 total;
 //   bs_views    per view: sorted-element range (from the compaction's view offsets), entry range
@@ -49,8 +49,8 @@ __device__ __forceinline__ bool bs_segment(const BsInfo* info, int nv, uint32_t 
     v = 0;
     for (int u = 1; u < nv; u++)
         if (info->segbase[u] <= seg) v = u;  // the last view starting at or before seg (empty views skipped)
-    q0 = info->ebase[v] + (seg - info->segbase[v]) * (uint32_t)BS_SEGE;
-    q1 = min(q0 + (uint32_t)BS_SEGE, info->ebase[v + 1]);
+    q0 = info->ebase[v] + (seg - info->segbase[v]) * info->sege;
+    q1 = min(q0 + info->sege, info->ebase[v + 1]);
     return true;
 }
 
@@ -154,14 +154,15 @@ __global__ void __launch_bounds__(256) bs_gather_kernel(const uint32_t* __restri
 // first tile: selection is view-major and the depth sort keeps views apart), entry bases,
 // segment table.
 __global__ void bs_views_kernel(const uint32_t* __restrict__ sel_offsets, int tiles_per_view,
-                                const uint32_t* __restrict__ offs, uint32_t nsel, int nv, BsInfo* info) {
+                                const uint32_t* __restrict__ offs, uint32_t nsel, int nv, uint32_t sege,
+                                BsInfo* info) {
     const int lane = threadIdx.x;
     uint32_t start = nsel;
     if (lane < nv) start = lane == 0 ? 0u : sel_offsets[(size_t)lane * tiles_per_view];
     const uint32_t eb = start > 0 ? offs[start - 1] : 0u;  // entries before the view
     uint32_t ee = __shfl_down_sync(FULL, eb, 1);
     if (lane == nv - 1) ee = offs[nsel - 1];
-    const uint32_t nseg = lane < nv ? (ee - eb + BS_SEGE - 1) / BS_SEGE : 0u;
+    const uint32_t nseg = lane < nv ? (ee - eb + sege - 1) / sege : 0u;
     uint32_t inc = nseg;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -177,6 +178,7 @@ __global__ void bs_views_kernel(const uint32_t* __restrict__ sel_offsets, int ti
         info->vstart[nv] = nsel;
         info->ebase[nv] = ee;
         info->segbase[nv] = inc;
+        info->sege = sege;
     }
 }
 
@@ -218,8 +220,10 @@ __global__ void __launch_bounds__(256) bs_colscan_kernel(const BsInfo* __restric
     const uint32_t per = (s1 - s0 + 7) / 8;
     const uint32_t a0 = min(s1, s0 + warp * per), a1 = min(s1, a0 + per);
     uint32_t sum = 0;
-    if (b < nb)
+    if (b < nb) {
+#pragma unroll 8
         for (uint32_t s = a0; s < a1; s++) sum += cnt[(size_t)s * nb + b];
+    }
     part[warp][lane] = sum;
     __syncthreads();
     uint32_t run = 0, tot = 0;
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(256) bs_colscan_kernel(const BsInfo* __restric
         tot += part[w][lane];
     }
     if (b >= nb) return;
+#pragma unroll 8
     for (uint32_t s = a0; s < a1; s++) {
         const uint32_t c = cnt[(size_t)s * nb + b];
         cnt[(size_t)s * nb + b] = run;
@@ -322,7 +327,24 @@ int bs_warps_per_cta(int nb) {
 
 }  // namespace
 
-size_t binsort_segments_max(int64_t entries, int nv) { return (size_t)((entries + BS_SEGE - 1) / BS_SEGE + nv); }
+// Entries per segment: BS_SEGE, or more for very large chunks, so that the segments (warps) stay
+// about one resident wave and the [segment][bin] matrix stays small (the column scan reads it
+// twice).
+static int g_segment_override = 0;  // scoup_diag_set_binsort_segment
+
+uint32_t binsort_segment_len(int64_t entries) {
+    if (g_segment_override > 0) return (uint32_t)g_segment_override;
+    const int64_t target = 148 * 48 * 16;  // (measured: longer segments cost the count and scatter more)
+    const int64_t len = std::max<int64_t>(BS_SEGE, ((entries + target - 1) / target + 255) / 256 * 256);
+    return (uint32_t)len;
+}
+
+void binsort_set_segment_override(int len) { g_segment_override = len > 0 ? (len + 31) / 32 * 32 : 0; }
+
+size_t binsort_segments_max(int64_t entries, int nv) {
+    const int64_t len = binsort_segment_len(entries);
+    return (size_t)((entries + len - 1) / len + nv);
+}
 
 void launch_binsort_gather(const uint32_t* sval_sorted, const uint32_t* tiles, int64_t nsel, uint32_t* offs,
                            BsInfo* info, cudaStream_t s) {
@@ -335,7 +357,8 @@ void launch_binsort(const uint32_t* sel_offsets, int tiles_per_view, const uint3
                     const uint32_t* sval_sorted, const uint2* rect, int64_t nsel, int64_t entries, int nv,
                     int bins_x, int nb, BsInfo* info, uint32_t* cnt, uint16_t* ebin, uint32_t* eel, uint2* ranges,
                     uint32_t* eval, cudaStream_t s) {
-    bs_views_kernel<<<1, 32, 0, s>>>(sel_offsets, tiles_per_view, offs, (uint32_t)nsel, nv, info);
+    bs_views_kernel<<<1, 32, 0, s>>>(sel_offsets, tiles_per_view, offs, (uint32_t)nsel, nv,
+                                     binsort_segment_len(entries), info);
     const int wpc = bs_warps_per_cta(nb);
     const size_t smem = (size_t)wpc * nb * sizeof(uint32_t);
     static size_t smem_set = 48 * 1024;

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "../../include/scoup_diag.h"
+#include "internal.cuh"
 
 namespace {
 
@@ -53,6 +54,15 @@ thread_local std::string g_diag_error;
 extern "C" {
 
 const char* scoup_diag_last_error(void) { return g_diag_error.c_str(); }
+
+int scoup_diag_set_binsort_segment(int entries_per_segment) {
+    if (entries_per_segment < 0 || entries_per_segment > (1 << 24)) {
+        g_diag_error = "entries_per_segment out of range";
+        return 1;
+    }
+    scoup::binsort_set_segment_override(entries_per_segment);
+    return 0;
+}
 
 int scoup_diag_red_rate(int device, int64_t buffer_bytes, int scattered, int vec4, int64_t reds_per_launch,
                         int launches, double* adds_per_s, double* ms_per_launch) {

@@ -102,12 +102,13 @@ struct ViewBuffers {
 
 // Segment table of the stable bin scatter (binsort.cu): view v's sorted elements are
 // [vstart[v], vstart[v+1]) and its flattened entries [ebase[v], ebase[v+1]), cut into runs of
-// BS_SEGE entries starting at segment segbase[v].
+// sege (>= BS_SEGE) entries starting at segment segbase[v].
 constexpr int BS_SEGE = 2048;
 struct BsInfo {
     uint32_t vstart[MAX_VB + 1];
     uint32_t ebase[MAX_VB + 1];
     uint32_t segbase[MAX_VB + 1];
+    uint32_t sege;             // entries per segment (binsort_segment_len)
     unsigned long long total;  // entries of the chunk (exact)
 };
 
@@ -399,6 +400,8 @@ void launch_depth_pass_near(PackedGaussians pg, int64_t G, const CamBatch& cams,
 void launch_preprocess(PackedGaussians pg, int64_t G, const CamBatch& cams, Binning bn, ViewBuffers vb,
                        int key_bits, int64_t nsel, cudaStream_t s);
 size_t binsort_segments_max(int64_t entries, int nv);
+uint32_t binsort_segment_len(int64_t entries);
+void binsort_set_segment_override(int len);
 void launch_binsort_gather(const uint32_t* sval_sorted, const uint32_t* tiles, int64_t nsel, uint32_t* offs,
                            BsInfo* info, cudaStream_t s);
 void launch_binsort(const uint32_t* sel_offsets, int tiles_per_view, const uint32_t* offs,

@@ -81,3 +81,11 @@ def test_sass_uses_global_reductions(lib):
     assert raster, "raster kernel not found in SASS"
     assert "REDG.E.ADD.F32" in raster
     assert "ATOMG.E.ADD.F32" not in raster
+
+
+def test_binsort_segment_override_validation(lib):
+    """scoup_diag_set_binsort_segment (include/scoup_diag.h): range check, host-only state."""
+    assert lib.scoup_diag_set_binsort_segment(-1) == 1
+    assert lib.scoup_diag_set_binsort_segment((1 << 24) + 1) == 1
+    assert lib.scoup_diag_set_binsort_segment(100) == 0
+    assert lib.scoup_diag_set_binsort_segment(0) == 0

@@ -112,6 +112,23 @@ def test_small_all_views_counters_and_one_context(dev, small_all_views):
     assert res["stats"]["batches"] == [-(-50 // res["stats"]["view_batch"]), 0]
 
 
+@pytest.mark.parametrize("seg", [32, 4096])
+def test_small_all_views_binning_segment_lengths(dev, small_all_views, seg):
+    """The binning's stable counting sort (DESIGN.md §5 a3) with forced warp-segment lengths: 32
+    entries (many segments per view, elements split across segment boundaries) and 4096 (the long
+    segments large chunks get); W/Z element-wise, codes and the exact contribution count."""
+    from paper_2605_13600_b200 import abi
+    cfg, scene, maps, codes, ora = small_all_views
+    abi.scoup_diag_set_binsort_segment(seg)
+    try:
+        res = run_production(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, host_maps=False,
+                             counters=True)
+    finally:
+        abi.scoup_diag_set_binsort_segment(0)
+    check(res, ora, cfg.K, 0.01)
+    assert res["stats"]["contributions"] == int(ora[2].sum())
+
+
 @pytest.fixture(scope="module")
 def outdoor_bands():
     """configs[3] at full size (3M Gaussians, L = 64, S = K = 8): 24 row bands of 24 rows, each
