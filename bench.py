@@ -593,7 +593,10 @@ def main():
                                     "frac_of_hbm_resident_rate": (red_rate / red_peak_hbm) if red_peak_hbm else None,
                                     "measured_peaks": red_peaks},
                          "peak_source": f"{sms} SMs x 128 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
-            "gpu_launches": int((st["kernel_launches"] + st["cub_launches"]) / max(1, args.steps)),
+            # the library's kernel launches in the timed region (its stats cover one step: they
+            # are reset with the accumulators at each step start)
+            "gpu_launches": int((st["kernel_launches"] + st["cub_launches"]) * args.steps),
+            "gpu_launches_per_step": int(st["kernel_launches"] + st["cub_launches"]),
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

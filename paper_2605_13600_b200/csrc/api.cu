@@ -474,7 +474,9 @@ void chunk_front(scoup_uplift* h, Ctx& c, const CallArgs& a, int64_t nsel) {
     CK(cub::DeviceScan::InclusiveSum(c.cub_tmp, need2, b.skey, b.skey, (int)nsel, c.s));
     CK(cudaMemcpyAsync(c.h_total, &b.binfo->total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s));
     h->kernel_launches += 2;
-    h->cub_launches += 2;
+    // CUB kernels: the onesweep sort (histogram, exclusive sum, one pass per 8 key bits) and the
+    // scan (init + scan)
+    h->cub_launches += 2 + (end_bit + 7) / 8 + 2;
 }
 
 // Near chunk: per view, the nearest ~near_frac of the visible Gaussians (a histogram bucket

@@ -550,15 +550,22 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PackedGaussians pg, int
                     double dca = ca, dcb = cb, dcc = cc;
                     double detc = dca * dcc - dcb * dcb;
                     if (detc > 0.0) {
+                        // half-widths m sqrt((conic^-1)_xx), m sqrt((conic^-1)_yy): the square
+                        // roots of the inverse's diagonal once, sqrt(m^2) per round (fp64
+                        // rounding far inside the 1.001 and +0.01 margins)
+                        const double inv = 1.0 / detc;
+                        const double sxx = sqrt(dcc * inv), syy = sqrt(dca * inv);
+                        const double kx = fabs((double)qa) + 0.5 * fabs((double)qb);
+                        const double ky = fabs((double)qc) + 0.5 * fabs((double)qb);
                         double yc = (double)ycut;
                         double ex = r, ey = r;
                         for (int it = 0; it < 3; it++) {
                             double m2 = -2.0 * 0.6931471805599453 * yc;
                             if (m2 <= 0.0) break;
-                            ex = fmin((double)r, sqrt(m2 * dcc / detc) * 1.001 + 0.01);
-                            ey = fmin((double)r, sqrt(m2 * dca / detc) * 1.001 + 0.01);
-                            double mq = (fabs((double)qa) + 0.5 * fabs((double)qb)) * ex * ex +
-                                        (fabs((double)qc) + 0.5 * fabs((double)qb)) * ey * ey;
+                            const double m = sqrt(m2);
+                            ex = fmin((double)r, m * sxx * 1.001 + 0.01);
+                            ey = fmin((double)r, m * syy * 1.001 + 0.01);
+                            double mq = kx * ex * ex + ky * ey * ey;
                             yc = (double)ycut - 0.01 - 2e-6 * mq;
                         }
                         hx = (float)ex;
