@@ -52,7 +52,7 @@ for rep in range(3):
 # device-resident add_views for reference
 md = maps.to(dev)
 cd = synth.Codes(codes_h.atoms.to(dev), codes_h.coefs.to(dev), codes.row0, codes.num_regions)
-gd = synth.Gaussians(*[a.to(dev) for a in g_h])
+gd = synth.Gaussians(*[a.to(dev) for a in (g_h.means, g_h.scales, g_h.rotations, g_h.opacities)])
 u = SparseUplift(gd, cfg.L, cfg.K, device=0, rows_padded=g.count)
 for rep in range(2):
     u.reset(); torch.cuda.synchronize(); t = time.perf_counter(); u.add_views(cams, md, cd); torch.cuda.synchronize()
