@@ -142,54 +142,76 @@ __device__ __forceinline__ void reach_fast(const float t[3], float s2max, const 
     asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(s2max * jf2 + K_LOWPASS));
     rb = 3.0f * sq * 1.002f + 1.0f + 1e-5f * (fabsf(fu) + fabsf(fv));
 }
-// (NaN fails every comparison; an infinite mean fails one side; an infinite radius keeps the
-// Gaussian -- conservative, the exact EWA of preprocess decides)
-__device__ __forceinline__ bool box_on_image(float mx, float my, float rb, const Camera& cam) {
-    return mx + rb >= 0.f && mx - rb <= (float)cam.width && my + rb >= 0.f && my - rb <= (float)cam.height;
-}
-__device__ __forceinline__ bool box_on_image(float mx, float my, float rb, float Wf, float Hf) {
-    return mx + rb >= 0.f && mx - rb <= Wf && my + rb >= 0.f && my - rb <= Hf;
-}
-
 // Stable compactions over the batch indices (below) and the depth pass share one tiling: tiles of
 // SEL_TILE Gaussians per view, 8 warps each owning SEL_ITEMS rounds of 32 consecutive Gaussians.
 constexpr int SEL_ITEMS = 16;
 constexpr int SEL_TILE = 256 * SEL_ITEMS;
 
 // Packed reach box in 16x16 tiles for the far-chunk predicate (x0 | x1 << 8 | y0 << 16 | y1 << 24;
-// x0 > x1: no tile); images up to 255 tiles a side (wider ones recompute in far_flags).
+// x0 > x1: no tile); images up to 255 tiles a side (wider ones recompute in the far predicate).
 constexpr uint32_t TRECT_EMPTY = 0x000000FFu;
-__device__ __forceinline__ uint32_t tile_rect(float mx, float my, float rb, int tiles_x, int tiles_y) {
-    // pixel x's centre x + 0.5 within [mx - rb, mx + rb]  <=>  x in [mx - rb - 0.5, mx + rb - 0.5]
-    // (cvt.rmi saturates: out-of-range and infinite bounds clamp like the exact floor would)
-    const int x0 = max(0, __float2int_rd((mx - rb - 0.5f) * (1.0f / TILE)));
-    const int x1 = min(tiles_x - 1, __float2int_rd((mx + rb - 0.5f) * (1.0f / TILE)));
-    const int y0 = max(0, __float2int_rd((my - rb - 0.5f) * (1.0f / TILE)));
-    const int y1 = min(tiles_y - 1, __float2int_rd((my + rb - 0.5f) * (1.0f / TILE)));
-    if (x0 > x1 || y0 > y1) return TRECT_EMPTY;
-    return (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
+
+// The depth pass's camera: the rows of [R|t], the focal lengths and their squares, and the
+// principal point in tile units ((c - 0.5) / 16), last tile indices.
+struct DepthCam {
+    float P[12];
+    float fx, fy, fx2, fy2, cxt, cyt;
+    int tx1, ty1;
+};
+__device__ __forceinline__ DepthCam depth_cam(const Camera& cam) {
+    DepthCam d;
+#pragma unroll
+    for (int k = 0; k < 12; k++) d.P[k] = cam.P[k];
+    d.fx = cam.fx;
+    d.fy = cam.fy;
+    d.fx2 = cam.fx * cam.fx;
+    d.fy2 = cam.fy * cam.fy;
+    d.cxt = (cam.cx - 0.5f) * (1.0f / TILE);
+    d.cyt = (cam.cy - 0.5f) * (1.0f / TILE);
+    d.tx1 = (cam.width + TILE - 1) / TILE - 1;
+    d.ty1 = (cam.height + TILE - 1) / TILE - 1;
+    return d;
 }
 
 // Depth code of Gaussian i in the view (V1, V2, the conservative on-screen test) and, when
-// visible, its packed reach box in 16x16 tiles.
-__device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const Camera& cam, float Wf, float Hf,
-                                               uint32_t none, int tiles_x, int tiles_y, bool want_rect,
+// visible, its packed reach box in 16x16 tiles.  The reach is reach_fast's bound (same terms, with
+// FMAs; its 0.2% + 1 px padding is far above their few-ulp differences), taken in tile units: the
+// tiles whose pixel centres x + 0.5 can lie within [mx - rb, mx + rb] are
+// floor((mx -+ rb - 0.5) / 16) = floor(fu / 16 + (cx - 0.5) / 16 -+ rb / 16) (cvt.rmi saturates:
+// out-of-range and infinite bounds clamp like the exact floor would).  Visible: the box clamped to
+// the image's tile grid is non-empty (a pixel centre of the grid lies within the reach) -- a
+// conservative superset of the pixels the exact EWA support can reach.  t[2] (the depth code) is
+// computed with the exact V1 operations.
+__device__ __forceinline__ uint32_t depth_code(const float4& A, float s2, const DepthCam& dc, uint32_t none,
                                                uint32_t& rect, bool& beyond) {
     uint32_t c = none;
     rect = TRECT_EMPTY;
     beyond = false;
     float t[3];
-    camera_space(A, cam, t);
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+        t[a] = add(add(add(mul(dc.P[4 * a + 0], A.x), mul(dc.P[4 * a + 1], A.y)), mul(dc.P[4 * a + 2], A.z)),
+                   dc.P[4 * a + 3]);
     if (t[2] > K_NEAR && A.w >= K_AMIN) {
-        float mx, my, rb;
-        reach_fast(t, s2, cam, mx, my, rb);
-        if (box_on_image(mx, my, rb, Wf, Hf)) {
+        const float iz = __fdividef(1.0f, t[2]);
+        const float u = t[0] * iz, v = t[1] * iz;
+        const float fu = dc.fx * u, fv = dc.fy * v;
+        const float jf2 = fmaf(dc.fx2, fmaf(u, u, 1.0f), dc.fy2 * fmaf(v, v, 1.0f)) * (iz * iz);
+        float sq;
+        asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(fmaf(s2, jf2, K_LOWPASS)));
+        const float rb = fmaf(3.006f, sq, fmaf(1e-5f, fabsf(fu) + fabsf(fv), 1.0f));
+        const float rt = rb * (1.0f / TILE);
+        const float ax = fmaf(fu, 1.0f / TILE, dc.cxt), ay = fmaf(fv, 1.0f / TILE, dc.cyt);
+        const int x0 = max(0, __float2int_rd(ax - rt)), x1 = min(dc.tx1, __float2int_rd(ax + rt));
+        const int y0 = max(0, __float2int_rd(ay - rt)), y1 = min(dc.ty1, __float2int_rd(ay + rt));
+        if (x0 <= x1 && y0 <= y1) {
             c = __float_as_uint(t[2]) - __float_as_uint(K_NEAR);
             if (!(c < none)) {  // beyond the host's depth bound for the batch (cannot happen)
                 beyond = true;
                 c = none;
+            } else {
+                rect = (uint32_t)x0 | ((uint32_t)x1 << 8) | ((uint32_t)y0 << 16) | ((uint32_t)y1 << 24);
             }
-            if (want_rect) rect = tile_rect(mx, my, rb, tiles_x, tiles_y);
         }
     }
     return c;
@@ -204,7 +226,7 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(PackedGaussians pg, int
     for (int k = threadIdx.x; k < NHIST; k += blockDim.x) sh[k] = 0;
     __syncthreads();
     const int view = blockIdx.y;
-    const Camera cam = cams.cam[view];
+    const DepthCam dc = depth_cam(cams.cam[view]);
     const uint32_t none = (1u << key_bits) - 1u;
     const int shift = key_bits > HIST_BITS ? key_bits - HIST_BITS : 0;
     const int64_t n = (G + HIST_SAMPLE - 1) / HIST_SAMPLE;
@@ -212,8 +234,7 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(PackedGaussians pg, int
         const int64_t i = k * HIST_SAMPLE;
         uint32_t rect;
         bool beyond;
-        const uint32_t c = depth_code(pg.a[i], pg.s2[i], cam, (float)cam.width, (float)cam.height, none, 0, 0, false,
-                                      rect, beyond);
+        const uint32_t c = depth_code(pg.a[i], pg.s2[i], dc, none, rect, beyond);
         if (c != none) atomicAdd(&sh[c >> shift], 1u);
     }
     __syncthreads();
@@ -221,65 +242,88 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(PackedGaussians pg, int
         if (sh[k]) atomicAdd(&hist[view * NHIST + k], sh[k]);
 }
 
-// One thread per (view, Gaussian), grid (tiles of SEL_TILE Gaussians, view): writes code[j]
-// (j = v*G + i) and the packed reach box, counts the visible Gaussians, and runs the count pass of
-// the near chunk's stable compaction in the same sweep (code < thr[v]: the predicate words and
-// tile counts sel_scan / sel_scatter take, laid out as sel_count_kernel's).  Off-screen Gaussians
-// (conservative reach misses the image) are invisible.
+// One thread per Gaussian and all views of the batch, grid (tiles of SEL_TILE Gaussians): writes
+// code[j] (j = v*G + i) and the packed reach box, counts the visible Gaussians, and runs the count
+// pass of the near chunk's stable compaction in the same sweep (code < thr[v]: the predicate words
+// and per-(view, tile) counts sel_scan / sel_scatter take, laid out as sel_count_kernel's).
+// Off-screen Gaussians (conservative reach misses the image) are invisible.  Each Gaussian is read
+// once per batch (groups of DP_GROUP items held in registers while the views loop, each camera
+// loaded once per group).  The far chunk's predicate reads only the reach box, so the box of an
+// invisible or near element is written empty (it can never be a far element).
+constexpr int DP_GROUP = 4;
 __global__ void __launch_bounds__(256) depth_pass_kernel(PackedGaussians pg, int64_t G, const CamBatch cams,
                                                          int key_bits, const uint32_t* __restrict__ thr,
                                                          uint32_t* __restrict__ code,
                                                          unsigned long long* visible_ctr, ErrorLatch err, int tiles_x,
                                                          int tiles_y, uint32_t* __restrict__ trect,
                                                          uint32_t* __restrict__ counts, uint32_t* __restrict__ bits) {
-    __shared__ uint32_t ws[8], wv[8];
-    const int view = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const Camera cam = cams.cam[view];  // (a register copy: no per-use parameter loads)
+    __shared__ uint32_t sbits[MAX_VB][8][SEL_ITEMS];  // predicate words (view, warp, item)
+    __shared__ uint32_t sn[MAX_VB][8];                // near counts (view, warp)
+    __shared__ uint32_t sthr[MAX_VB], wv[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nv = cams.n;
     const uint32_t none = (1u << key_bits) - 1u;
-    const uint32_t tv = thr[view];
-    const float Wf = (float)cam.width, Hf = (float)cam.height;
-    const int64_t base = (int64_t)blockIdx.x * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
-    const int64_t tile = (int64_t)view * gridDim.x + blockIdx.x;
-    // this thread's Gaussians i = base + 32 it and their (view, Gaussian) slots, as offsets
-    const float4* pa = pg.a + base;
-    const float* ps = pg.s2 + base;
-    uint32_t* pc = code + (int64_t)view * G + base;
-    uint32_t* pr = trect ? trect + (int64_t)view * G + base : nullptr;
-    const int nit = (int)max((int64_t)0, min((int64_t)SEL_ITEMS, (G - base + 31) / 32));  // items with i < G
-    uint32_t n = 0, nvis = 0, word = 0;
-#pragma unroll 8
-    for (int it = 0; it < SEL_ITEMS; it++) {
-        bool near = false;
-        if (it < nit) {
-            uint32_t rect;
-            bool beyond;
-            const uint32_t c = depth_code(pa[32 * it], ps[32 * it], cam, Wf, Hf, none, tiles_x, tiles_y, pr != nullptr,
-                                          rect, beyond);
-            if (beyond) latch_error(err, ERR_DEPTHKEY, (int64_t)view * G + base + 32 * it);
-            pc[32 * it] = c;
-            if (pr) pr[32 * it] = rect;
-            nvis += c != none ? 1u : 0u;
-            near = c < tv && c != none;
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, near);
-        n += __popc(b);
-        if (lane == it) word = b;  // the warp's 16 predicate words, one per lane, for the scatter
-    }
-    if (lane < SEL_ITEMS) bits[(tile * 8 + warp) * SEL_ITEMS + lane] = word;
-    nvis = __reduce_add_sync(0xffffffffu, nvis);
-    if (lane == 0) {
-        ws[warp] = n;
-        wv[warp] = nvis;
-    }
+    if (threadIdx.x < nv) sthr[threadIdx.x] = thr[threadIdx.x];
+    if (lane < nv) sn[lane][warp] = 0u;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0, vis = 0;
+    const int64_t base = (int64_t)blockIdx.x * SEL_TILE + warp * (SEL_ITEMS * 32) + lane;
+    const int nit = (int)max((int64_t)0, min((int64_t)SEL_ITEMS, (G - base + 31) / 32));  // items with i < G
+    uint32_t nvis = 0;
+    for (int g = 0; g < SEL_ITEMS; g += DP_GROUP) {
+        float4 A[DP_GROUP];
+        float s2[DP_GROUP];
 #pragma unroll
-        for (int w = 0; w < 8; w++) {
-            tot += ws[w];
-            vis += wv[w];
+        for (int u = 0; u < DP_GROUP; u++) {
+            if (g + u < nit) {
+                A[u] = pg.a[base + 32 * (g + u)];
+                s2[u] = pg.s2[base + 32 * (g + u)];
+            } else {
+                A[u] = make_float4(0.f, 0.f, 0.f, -1.f);  // (fails the opacity test: invisible)
+                s2[u] = 0.f;
+            }
         }
-        counts[tile] = tot;
+        for (int v = 0; v < nv; v++) {
+            const DepthCam dc = depth_cam(cams.cam[v]);  // (warp-uniform: one register copy per group)
+            const uint32_t tv = sthr[v];
+            const int64_t j0 = (int64_t)v * G + base;
+            uint32_t nn = 0;  // near elements of the warp's items in this group
+#pragma unroll
+            for (int u = 0; u < DP_GROUP; u++) {
+                const int it = g + u;
+                uint32_t rect;
+                bool beyond;
+                const uint32_t c = depth_code(A[u], s2[u], dc, none, rect, beyond);
+                const bool near = c < tv;  // (tv <= none: the invisible code is never near)
+                if (it < nit) {
+                    if (beyond) latch_error(err, ERR_DEPTHKEY, j0 + 32 * it);
+                    code[j0 + 32 * it] = c;
+                    if (trect) trect[j0 + 32 * it] = near ? TRECT_EMPTY : rect;  // (rect is empty when invisible)
+                    nvis += c != none ? 1u : 0u;
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, near);
+                if (lane == 0) sbits[v][warp][it] = b;
+                nn += (uint32_t)__popc(b);
+            }
+            if (lane == 0) sn[v][warp] += nn;
+        }
+    }
+    nvis = __reduce_add_sync(0xffffffffu, nvis);
+    if (lane == 0) wv[warp] = nvis;
+    __syncthreads();
+    // the (view, tile) predicate words and counts: tile = v * gridDim.x + blockIdx.x
+    for (int k = threadIdx.x; k < nv * 8 * SEL_ITEMS; k += blockDim.x) {
+        const int v = k / (8 * SEL_ITEMS), r = k - v * (8 * SEL_ITEMS);
+        bits[((int64_t)v * gridDim.x + blockIdx.x) * (8 * SEL_ITEMS) + r] = (&sbits[v][0][0])[r];
+    }
+    if (threadIdx.x < nv) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) tot += sn[threadIdx.x][w];
+        counts[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = tot;
+    }
+    if (threadIdx.x == 0) {
+        uint32_t vis = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) vis += wv[w];
         if (vis) atomicAdd(visible_ctr, (unsigned long long)vis);
     }
 }
@@ -331,20 +375,21 @@ struct FarSel {
     int tiles_x, tiles_y;
     PackedGaussians pg;
     const CamBatch* cams;    // device copy (recompute path)
-    // both words loaded unconditionally (coalesced; the branch-free loads of a thread's items
-    // can all be in flight at once)
+    // With packed boxes only the box is loaded: the depth pass wrote it empty for invisible and
+    // near elements, so a non-empty box is a visible code at or beyond the split.  Loads are
+    // unconditional (coalesced; the branch-free loads of a thread's items can all be in flight).
     __device__ __forceinline__ uint2 load(int view, int64_t i) const {
         const int64_t j = (int64_t)view * G + i;
-        return make_uint2(code[j], trect ? trect[j] : 0u);
+        return trect ? make_uint2(0u, trect[j]) : make_uint2(code[j], 0u);
     }
     __device__ __forceinline__ bool test(int view, int64_t i, uint2 v) const {
-        const uint32_t c = v.x;
-        if (c == none || c < thr[view]) return false;
         int x0, x1, y0, y1;
         if (trect) {
             const uint32_t r = v.y;
             x0 = (int)(r & 255u); x1 = (int)((r >> 8) & 255u); y0 = (int)((r >> 16) & 255u); y1 = (int)(r >> 24);
         } else {
+            const uint32_t c = v.x;
+            if (c == none || c < thr[view]) return false;
             const Camera& cam = cams->cam[view];
             float t[3];
             camera_space(pg.a[i], cam, t);
@@ -690,6 +735,45 @@ __device__ __forceinline__ void topk_insert(float (&bv)[KMAX], uint32_t (&ba)[KM
     }
 }
 
+// The 8th largest of 16 values: both halves sorted descending (the optimal 19-comparator network
+// for 8), then the top 8 of the union are max(a_i, b_(7-i)) and their minimum is the 8th largest.
+__device__ __forceinline__ float eighth_of_16(float (&m)[16]) {
+    constexpr int net[19][2] = {{0, 2}, {1, 3}, {4, 6}, {5, 7}, {0, 4}, {1, 5}, {2, 6}, {3, 7}, {0, 1}, {2, 3},
+                                {4, 5}, {6, 7}, {2, 4}, {3, 5}, {1, 4}, {3, 6}, {1, 2}, {3, 4}, {5, 6}};
+#pragma unroll
+    for (int h = 0; h < 16; h += 8)
+#pragma unroll
+        for (int k = 0; k < 19; k++) {
+            const float a = m[h + net[k][0]], b = m[h + net[k][1]];
+            m[h + net[k][0]] = fmaxf(a, b);
+            m[h + net[k][1]] = fminf(a, b);
+        }
+    float t = fmaxf(m[0], m[15]);
+#pragma unroll
+    for (int i = 1; i < 8; i++) t = fminf(t, fmaxf(m[i], m[15 - i]));
+    return t;
+}
+
+// bit 4 (c4 - ca) + u: value u of float4 column c4 in [ca, cb) is >= tp
+__device__ __forceinline__ uint32_t candidate_bits(const float4* row, int ca, int cb, float tp) {
+    // set.ge gives an all-ones / zero word per value; each bit is one AND-OR (LOP3) into the mask
+    auto ge = [](float v, float t) {
+        uint32_t r;
+        asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(v), "f"(t));
+        return r;
+    };
+    uint32_t m = 0u;
+    for (int c4 = ca; c4 < cb; c4++) {
+        const float4 v4 = row[c4];
+        const int sh = 4 * (c4 - ca);
+        m |= ge(v4.x, tp) & (1u << sh);
+        m |= ge(v4.y, tp) & (2u << sh);
+        m |= ge(v4.z, tp) & (4u << sh);
+        m |= ge(v4.w, tp) & (8u << sh);
+    }
+    return m;
+}
+
 #ifndef SCOUP_TOPK_ROWS
 #define SCOUP_TOPK_ROWS 128
 #endif
@@ -775,7 +859,18 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
         // network -- in atom order, so ties keep the lower atom (strict >): the same selection and
         // order as inserting every value.
         float tau = 0.f;
-        if (L >= K) {
+        if (LC == 16 && KMAX == 8) {
+            // L = 64, K <= 8: the maxima of the 16 float4 groups are 16 distinct elements, so at
+            // least 8 >= K values are >= the 8th largest of them (~the row's 84th percentile for
+            // dense rows, against ~73rd for the minimum of K group maxima): fewer candidates
+            float m[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 16; c4++) {
+                const float4 v4 = row[c4];
+                m[c4] = fmaxf(fmaxf(v4.x, v4.y), fmaxf(v4.z, v4.w));
+            }
+            tau = eighth_of_16(m);
+        } else if (L >= K) {
             const int gs = L / K;
             tau = __int_as_float(0x7f800000);
             if ((gs & 3) == 0) {  // float4 groups (conflict-free LDS.128 on the padded rows)
@@ -798,17 +893,12 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
                 }
             }
         }
+        // candidates: v >= tau and v > 0, i.e. v >= max(tau, the smallest positive float)
+        const float tp = fmaxf(tau, __int_as_float(1));
         for (int c0 = 0; c0 < L4; c0 += 16) {  // chunks of 64 atoms: a candidate bit mask each
-            unsigned long long cm = 0ull;
-            const int c1 = min(L4, c0 + 16);
-            for (int c4 = c0; c4 < c1; c4++) {
-                const float4 v4 = row[c4];
-                const int sh = 4 * (c4 - c0);
-                cm |= (unsigned long long)((v4.x > 0.f && v4.x >= tau) ? 1u : 0u) << sh;
-                cm |= (unsigned long long)((v4.y > 0.f && v4.y >= tau) ? 2u : 0u) << sh;
-                cm |= (unsigned long long)((v4.z > 0.f && v4.z >= tau) ? 4u : 0u) << sh;
-                cm |= (unsigned long long)((v4.w > 0.f && v4.w >= tau) ? 8u : 0u) << sh;
-            }
+            const uint32_t lo = candidate_bits(row, c0, min(L4, c0 + 8), tp);  // (two 32-bit halves)
+            const uint32_t hi = candidate_bits(row, c0 + 8, min(L4, c0 + 16), tp);
+            unsigned long long cm = ((unsigned long long)hi << 32) | lo;
             while (cm) {
                 const int bit = __ffsll((long long)cm) - 1;
                 cm &= cm - 1ull;
@@ -822,6 +912,9 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
 #pragma unroll
     for (int s = 0; s < KMAX; s++)
         if (s < K) sum = __fadd_rn(sum, bv[s]);
+    // w = v / sum as v * (1 / sum): two roundings (<= 1.5 ulp, inside Eq. 6's fp32 tolerance) and
+    // monotone in v, so the stored coefficients keep the selection's descending order
+    const float inv = __frcp_rn(sum);
     if (entropy && r < rows) entropy[r] = hs > 0.f ? fmaxf(0.f, logf(hs) - hw / hs) : __int_as_float(0x7fc00000);
     if (2 * K > L + 4) {  // (codes wider than half a staged row: direct stores)
         if (r < rows) {
@@ -830,7 +923,7 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
                 if (s < K) {
                     bool keep = bv[s] > 0.f;
                     atoms[r * K + s] = keep ? ba[s] : NONE;
-                    coefs[r * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+                    coefs[r * K + s] = keep ? __fmul_rn(bv[s], inv) : 0.f;
                 }
             }
         }
@@ -846,7 +939,7 @@ __global__ void __launch_bounds__(TOPK_ROWS) topk_tile_kernel(PeerRows peers, in
         if (s < K) {
             bool keep = bv[s] > 0.f;
             oa[t * K + s] = keep ? ba[s] : NONE;
-            oc[t * K + s] = keep ? __fdiv_rn(bv[s], sum) : 0.f;
+            oc[t * K + s] = keep ? __fmul_rn(bv[s], inv) : 0.f;
         }
     }
     __syncthreads();
@@ -885,6 +978,9 @@ __global__ void __launch_bounds__(128) topk_kernel_scalar(const float* __restric
 #pragma unroll
     for (int s = 0; s < KMAX; s++)
         if (s < K) sum = __fadd_rn(sum, bv[s]);
+    // w = v / sum as v * (1 / sum): two roundings (<= 1.5 ulp, inside Eq. 6's fp32 tolerance) and
+    // monotone in v, so the stored coefficients keep the selection's descending order
+    const float inv = __frcp_rn(sum);
 #pragma unroll
     for (int s = 0; s < KMAX; s++) {
         if (s < K) {
@@ -943,8 +1039,8 @@ void launch_depth_pass_near(PackedGaussians pg, int64_t G, const CamBatch& cams,
     const int64_t tiles = (int64_t)grid.x * grid.y;
     uint32_t* bits = counts + tiles;
     const bool packed = bn.tiles_x <= 255 && bn.tiles_y <= 255;
-    depth_pass_kernel<<<grid, 256, 0, s>>>(pg, G, cams, key_bits, thr, code, visible_ctr, err, bn.tiles_x, bn.tiles_y,
-                                           packed ? trect : nullptr, counts, bits);
+    depth_pass_kernel<<<grid.x, 256, 0, s>>>(pg, G, cams, key_bits, thr, code, visible_ctr, err, bn.tiles_x, bn.tiles_y,
+                                             packed ? trect : nullptr, counts, bits);
     sel_scan_kernel<<<1, 1024, 0, s>>>(counts, (int)tiles, nsel);
     sel_scatter_kernel<<<grid, 256, 0, s>>>(G, counts, bits, sel);
 }
