@@ -33,6 +33,13 @@ int scoup_diag_red_rate(int device, int64_t buffer_bytes, int scattered, int vec
  * entries_per_segment is negative or above 2^24. */
 int scoup_diag_set_binsort_segment(int entries_per_segment);
 
+/* Region slots per 16x16 tile of the fused raster kernel (DESIGN.md §5 a4; process-wide): the
+ * kernel exists with 4 and with 8 shared-sum slots (tiles meeting more regions aggregate per
+ * pixel); 0 restores the adaptive choice (4 when every view of the batch averages >= 64 x 64 px
+ * per region, else 8), 4 or 8 forces a variant (tests: both variants on every configuration).
+ * Returns 0, or 1 for any other value. */
+int scoup_diag_set_raster2_slots(int slots);
+
 /* Thread-local message of the last failing diag call ("" if none). */
 const char *scoup_diag_last_error(void);
 

@@ -56,7 +56,7 @@ EXPORTS = ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_vi
            "scoup_sc_init", "scoup_sc_kmeans", "scoup_sc_set_state", "scoup_sc_get_state", "scoup_sc_train",
            "scoup_sc_encode", "scoup_sc_free",
            # include/scoup_diag.h (measurement helpers)
-           "scoup_diag_red_rate", "scoup_diag_set_binsort_segment", "scoup_diag_last_error"]
+           "scoup_diag_red_rate", "scoup_diag_set_binsort_segment", "scoup_diag_set_raster2_slots", "scoup_diag_last_error"]
 
 _lib = None
 
@@ -107,6 +107,8 @@ def lib():
         L.scoup_diag_last_error.restype = C.c_char_p
         L.scoup_diag_set_binsort_segment.argtypes = [C.c_int]
         L.scoup_diag_set_binsort_segment.restype = C.c_int
+        L.scoup_diag_set_raster2_slots.argtypes = [C.c_int]
+        L.scoup_diag_set_raster2_slots.restype = C.c_int
         for name in ["scoup_uplift_init", "scoup_uplift_init_levels", "scoup_uplift_add_views",
                      "scoup_uplift_add_views_levels", "scoup_uplift_finalize_topk", "scoup_uplift_finalize_topk_level",
                      "scoup_uplift_render_views", "scoup_uplift_decode",
@@ -354,6 +356,13 @@ def scoup_diag_red_rate(device: int, buffer_bytes: int, scattered: bool, vec4: b
     if st != 0:
         raise ScoupError(st, lib().scoup_diag_last_error().decode())
     return rate.value, ms.value
+
+
+def scoup_diag_set_raster2_slots(slots: int) -> None:
+    """include/scoup_diag.h: force the fused raster's 4- or 8-slot variant (0: adaptive)."""
+    st = lib().scoup_diag_set_raster2_slots(int(slots))
+    if st != 0:
+        raise ScoupError(st, lib().scoup_diag_last_error().decode())
 
 
 def scoup_diag_set_binsort_segment(entries_per_segment: int) -> None:

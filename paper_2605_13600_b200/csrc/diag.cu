@@ -64,6 +64,15 @@ int scoup_diag_set_binsort_segment(int entries_per_segment) {
     return 0;
 }
 
+int scoup_diag_set_raster2_slots(int slots) {
+    if (slots != 0 && slots != 4 && slots != 8) {
+        g_diag_error = "slots must be 0 (adaptive), 4 or 8";
+        return 1;
+    }
+    scoup::raster2_set_slots_override(slots);
+    return 0;
+}
+
 int scoup_diag_red_rate(int device, int64_t buffer_bytes, int scattered, int vec4, int64_t reds_per_launch,
                         int launches, double* adds_per_s, double* ms_per_launch) {
     g_diag_error.clear();

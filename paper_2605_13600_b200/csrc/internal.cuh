@@ -463,6 +463,7 @@ void launch_raster(const RasterParams& p, cudaStream_t s);
 // two pixels per thread (raster2.cu): the single-level sparse-code path (nlev == 1, !dense)
 bool raster2_supported(const RasterParams& p);
 void launch_raster2(const RasterParams& p, cudaStream_t s);
+void raster2_set_slots_override(int slots);  // 0: adaptive (scoup_diag_set_raster2_slots)
 void launch_render(const RasterParams& p, cudaStream_t s);
 
 void launch_topk(const float* W, int64_t rows, int64_t valid_rows, int L, int K, uint32_t* atoms, float* coefs,

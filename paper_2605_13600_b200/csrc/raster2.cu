@@ -24,6 +24,9 @@
 //
 // The per-thread transmittance uses the "dead below 1e-4" convention of raster.cu (a pixel is
 // finished once T < 1e-4; DESIGN.md §4 R9).
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace scoup {
@@ -35,24 +38,35 @@ constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;   // unassigned or outside the image
 constexpr uint32_t SLOT_EMPTY = 0xFFFFFFFEu;  // slot-table sentinel
 constexpr int R2T = 128;                      // threads per CTA (4 warps, 2 pixels each)
 constexpr int R2W = R2T / 32;
-constexpr int R2Q = 256;                      // ring capacity (>= 63 + 128 records in flight)
+#ifndef RASTER2_RING
+#define RASTER2_RING 192                      // ring capacity (>= 63 + 128 records in flight; a multiple of 32)
+#endif
+constexpr int R2Q = RASTER2_RING;
 #ifndef RASTER2_NSUB
 #define RASTER2_NSUB 2                        // sub-batches of BATCH records per barrier
 #endif
 #ifndef RASTER2_SLOTS
 #define RASTER2_SLOTS 8                       // distinct regions per tile on the shared-sum path (more: per-pixel path)
 #endif
+#ifndef RASTER2_SLOTS_FEW
+#define RASTER2_SLOTS_FEW 4                   // ... of the small-footprint variant for views with large regions
+#endif
 constexpr int R2SB = RASTER2_NSUB * BATCH;    // records per super-batch (one barrier, one flush)
-constexpr int R2S = RASTER2_SLOTS;
 constexpr int RG = 8;                         // records per warp-uniform group (and per reduction)
 #ifndef RASTER2_MIN_BLOCKS
-#define RASTER2_MIN_BLOCKS 6
+#define RASTER2_MIN_BLOCKS 7
 #endif
 
 static_assert(BATCH == 32 && (R2SB & (R2SB - 1)) == 0 && R2SB <= R2T, "sub-batches of one record per lane");
-static_assert(R2S <= MAX_SLOTS, "slot table");
-static_assert(R2Q >= R2SB - 1 + R2T, "ring holds a round on top of a partial super-batch");
+static_assert(RASTER2_SLOTS <= MAX_SLOTS && RASTER2_SLOTS_FEW <= RASTER2_SLOTS, "slot table");
+static_assert(R2Q >= R2SB - 1 + R2T && R2Q % BATCH == 0, "ring holds a round on top of a partial super-batch");
+// ring position of x < 2 R2Q (every use: head < R2Q plus less than R2SB + R2T)
+__device__ __forceinline__ uint32_t ring_wrap(uint32_t x) {
+    if ((R2Q & (R2Q - 1)) == 0) return x & (uint32_t)(R2Q - 1);
+    return x >= (uint32_t)R2Q ? x - (uint32_t)R2Q : x;
+}
 
+template <int R2S>
 struct __align__(16) R2Smem {
     float4 rp[R2Q];   // (mx, my, r, o)
     float4 rq[R2Q];   // (qa, qb, qc, ycut)
@@ -140,10 +154,10 @@ __device__ __noinline__ void overflow_red1(float* W, float* Z, const uint32_t* a
     }
 }
 
-template <bool COUNT>
+template <bool COUNT, int R2S>
 __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const RasterParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    R2Smem& sm = *reinterpret_cast<R2Smem*>(smem_raw);
+    R2Smem<R2S>& sm = *reinterpret_cast<R2Smem<R2S>*>(smem_raw);
     const int ntiles = p.bn.tiles_x * p.bn.tiles_y;
     const int view = blockIdx.x / ntiles, tile = blockIdx.x - view * ntiles;
     const int tx = tile % p.bn.tiles_x, ty = tile / p.bn.tiles_x;
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                 tot += c;
             }
             if (acc) {
-                const uint32_t pos = (q_head + q_count + off + __popc(bal & lanemask_lt)) & (R2Q - 1);
+                const uint32_t pos = ring_wrap(q_head + q_count + off + __popc(bal & lanemask_lt));
                 sm.rp[pos] = r0;
                 sm.rq[pos] = r1;
                 sm.re[pos] = r2;
@@ -304,12 +318,12 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
         if (n % BATCH) {
             // the tile's last, partial sub-batch: blank the stale ring slots after it (a negative
             // support radius fails every square test)
-            if ((uint32_t)t >= n && t < nsub * BATCH) sm.rp[(q_head + (uint32_t)t) & (R2Q - 1)].z = -1.0f;
+            if ((uint32_t)t >= n && t < nsub * BATCH) sm.rp[ring_wrap(q_head + (uint32_t)t)].z = -1.0f;
             __syncthreads();
         }
 #pragma unroll 1
         for (int sb = 0; sb < nsub; sb++) {
-            const uint32_t sh = (q_head + (uint32_t)(sb * BATCH)) & (R2Q - 1);  // contiguous: sh % 32 == 0
+            const uint32_t sh = ring_wrap(q_head + (uint32_t)(sb * BATCH));  // contiguous: sh % 32 == 0
             const uint32_t nsb = min((uint32_t)BATCH, n - (uint32_t)(sb * BATCH));
             const bool warp_done = __all_sync(FULL, !(TA >= K_TMIN) && !(TB >= K_TMIN));
             bool rel = false;
@@ -419,7 +433,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
             for (int w = 0; w < R2W; w++) ws[w] = sm.wslot[w];
             // ---- flush: S reds per (slot, record) into W, one per record into Z (sum over slots)
             const int ncol = nsub * BATCH;
-            auto gid_of = [&](int j) { return __float_as_uint(sm.re[(q_head + (uint32_t)j) & (R2Q - 1)].z); };
+            auto gid_of = [&](int j) { return __float_as_uint(sm.re[ring_wrap(q_head + (uint32_t)j)].z); };
             const int nitems = nslot * R2SB * S;
             for (int i = t; i < nitems; i += R2T) {
                 const uint32_t u = s_log2 >= 0 ? (uint32_t)i >> s_log2 : __umulhi((uint32_t)i, s_magic);  // (slot, record)
@@ -450,7 +464,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
             for (int i = t; i < nslot * R2SB; i += R2T) sm.acc[bz][i] = 0.f;
             for (int i = t; i < R2W * R2SB; i += R2T) (&sm.accw[bz][0][0])[i] = 0.f;
         }
-        q_head = (q_head + n) & (R2Q - 1);
+        q_head = ring_wrap(q_head + n);
         q_count -= n;
         buf = buf == 2 ? 0 : buf + 1;
         if (alive == 0) break;
@@ -492,18 +506,48 @@ bool raster2_supported(const RasterParams& p) {
     return p.nlev == 1 && !p.dense && p.S <= MAX_S;
 }
 
+// Slots per tile.  The variant with RASTER2_SLOTS_FEW slots has the smaller shared-memory
+// footprint (27.9 KB against 30.9 KB per CTA: the front kernels of the other pipeline context fit
+// next to 7 resident raster CTAs sooner, measured -2 ms per outdoor step); it serves batches
+// whose regions average at least 64 x 64 px (4 x 4 tiles: a tile then rarely meets more than 4
+// regions -- tiles that do take the per-pixel path in either variant).  SCOUP_RASTER2_SLOTS
+// or scoup_diag_set_raster2_slots (4 or 8) forces one variant.
+static int g_slots_override = -1;  // scoup_diag_set_raster2_slots (-1: SCOUP_RASTER2_SLOTS, else adaptive)
+
+static int raster2_slots(const RasterParams& p) {
+    if (g_slots_override < 0) {
+        const char* e = getenv("SCOUP_RASTER2_SLOTS");
+        g_slots_override = e ? std::max(0, atoi(e)) : 0;
+    }
+    if (g_slots_override > 0) return g_slots_override <= RASTER2_SLOTS_FEW ? RASTER2_SLOTS_FEW : RASTER2_SLOTS;
+    const int64_t area = (int64_t)p.width * p.height;
+    for (int v = 0; v < p.nviews; v++)
+        if ((int64_t)p.num_regions[v][0] * 4096 > area) return RASTER2_SLOTS;
+    return RASTER2_SLOTS_FEW;
+}
+
+template <int R2S>
+static void launch_raster2_slots(const RasterParams& p, int nblocks, cudaStream_t s) {
+    static_assert(RASTER2_MIN_BLOCKS * (sizeof(R2Smem<R2S>) + 1024) <= 228 * 1024, "shared memory per SM");
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(raster2_kernel<true, R2S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(R2Smem<R2S>));
+        cudaFuncSetAttribute(raster2_kernel<false, R2S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(R2Smem<R2S>));
+        attr_set = true;
+    }
+    if (p.count_tests) raster2_kernel<true, R2S><<<nblocks, R2T, sizeof(R2Smem<R2S>), s>>>(p);
+    else raster2_kernel<false, R2S><<<nblocks, R2T, sizeof(R2Smem<R2S>), s>>>(p);
+}
+
 void launch_raster2(const RasterParams& p, cudaStream_t s) {
     const int nblocks = p.bn.tiles_x * p.bn.tiles_y * p.nviews;
     if (nblocks <= 0) return;
-    static_assert(RASTER2_MIN_BLOCKS * (sizeof(R2Smem) + 1024) <= 228 * 1024, "shared memory per SM");
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(raster2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(R2Smem));
-        cudaFuncSetAttribute(raster2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(R2Smem));
-        attr_set = true;
-    }
-    if (p.count_tests) raster2_kernel<true><<<nblocks, R2T, sizeof(R2Smem), s>>>(p);
-    else raster2_kernel<false><<<nblocks, R2T, sizeof(R2Smem), s>>>(p);
+    if (raster2_slots(p) == RASTER2_SLOTS_FEW) launch_raster2_slots<RASTER2_SLOTS_FEW>(p, nblocks, s);
+    else launch_raster2_slots<RASTER2_SLOTS>(p, nblocks, s);
 }
+
+void raster2_set_slots_override(int slots) { g_slots_override = slots > 0 ? slots : 0; }
 
 }  // namespace scoup

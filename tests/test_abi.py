@@ -83,6 +83,15 @@ def test_sass_uses_global_reductions(lib):
     assert "ATOMG.E.ADD.F32" not in raster
 
 
+def test_raster2_slots_override_validation(lib):
+    """scoup_diag_set_raster2_slots (include/scoup_diag.h): 0, 4 or 8 only, host-only state."""
+    for bad in (-1, 1, 5, 16):
+        assert lib.scoup_diag_set_raster2_slots(bad) == 1
+    assert lib.scoup_diag_set_raster2_slots(4) == 0
+    assert lib.scoup_diag_set_raster2_slots(8) == 0
+    assert lib.scoup_diag_set_raster2_slots(0) == 0
+
+
 def test_binsort_segment_override_validation(lib):
     """scoup_diag_set_binsort_segment (include/scoup_diag.h): range check, host-only state."""
     assert lib.scoup_diag_set_binsort_segment(-1) == 1

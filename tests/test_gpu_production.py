@@ -129,6 +129,26 @@ def test_small_all_views_binning_segment_lengths(dev, small_all_views, seg):
     assert res["stats"]["contributions"] == int(ora[2].sum())
 
 
+@pytest.mark.parametrize("slots", [4, 8])
+def test_small_all_views_raster_slot_variants(dev, small_all_views, slots):
+    """The fused raster's 4- and 8-slot variants (DESIGN.md §5 a4), each forced on configs[1]
+    (64 Voronoi regions on 512 x 384: with 4 slots many tiles meet more regions than slots and
+    aggregate per pixel): W/Z element-wise, codes, the exact contribution count; then the
+    production kernel of the same variant."""
+    from paper_2605_13600_b200 import abi
+    cfg, scene, maps, codes, ora = small_all_views
+    abi.scoup_diag_set_raster2_slots(slots)
+    try:
+        res = run_production(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, host_maps=False,
+                             counters=True)
+        res2 = run_production(scene.gaussians, scene.cameras, maps, codes, cfg.L, cfg.K, host_maps=False)
+    finally:
+        abi.scoup_diag_set_raster2_slots(0)
+    check(res, ora, cfg.K, 0.01)
+    assert res["stats"]["contributions"] == int(ora[2].sum())
+    check(res2, ora, cfg.K, 0.01)
+
+
 @pytest.fixture(scope="module")
 def outdoor_bands():
     """configs[3] at full size (3M Gaussians, L = 64, S = K = 8): 24 row bands of 24 rows, each
@@ -168,6 +188,23 @@ def test_outdoor_full_size_bands_exact_counts(dev, outdoor_bands):
     res = run_production(scene.gaussians, cams, maps, codes, cfg.L, cfg.K, host_maps=False, counters=True)
     check(res, ora, cfg.K, 1e-3)
     assert res["stats"]["contributions"] == int(ora[2].sum())
+
+
+def test_outdoor_full_size_bands_four_slot_variant(dev, outdoor_bands):
+    """bench.py's full outdoor views (128 regions on 1600 x 1066) take the 4-slot raster variant;
+    the 24-row band cameras here would pick 8 slots by their own area, so it is forced: production
+    kernel element-wise, then the instrumented kernel's exact contribution count."""
+    from paper_2605_13600_b200 import abi
+    cfg, scene, cams, maps, codes, ora = outdoor_bands
+    abi.scoup_diag_set_raster2_slots(4)
+    try:
+        res = run_production(scene.gaussians, cams, maps, codes, cfg.L, cfg.K, host_maps=False)
+        res2 = run_production(scene.gaussians, cams, maps, codes, cfg.L, cfg.K, host_maps=False, counters=True)
+    finally:
+        abi.scoup_diag_set_raster2_slots(0)
+    check(res, ora, cfg.K, 1e-3)
+    check(res2, ora, cfg.K, 1e-3)
+    assert res2["stats"]["contributions"] == int(ora[2].sum())
 
 
 def test_finalize_entropy_host_output_rejected(dev, tiny_scene):
