@@ -284,8 +284,9 @@ void ctx_reserve(Ctx& c, int64_t G, int B, int64_t pixels, int64_t tiles) {
         void* ptrs[] = {b.code, b.sel, b.trect, b.selcnt};
         for (void* p : ptrs) dfree(p, c.s);
 #define RG(f) { dalloc(&b.f, (size_t)n, c.s); }
-        RG(code) RG(sel) RG(trect)
+        RG(sel) RG(trect)
 #undef RG
+        dalloc(&b.code, (size_t)n + 4, c.s);  // (preprocess reads the aligned 16 B holding a code)
         dalloc(&b.selcnt, select_counts_needed(G, MAX_VB) + 1, c.s);
         c.g_cap = (size_t)n;
     }
@@ -881,6 +882,11 @@ scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num
         h->K = K;
         h->nlev = num_levels;
         CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+        if (const char* e = getenv("SCOUP_CACHE_CONFIG")) {  // (A/B) device-wide L1 / shared-memory preference
+            const int m = atoi(e);
+            CK(cudaDeviceSetCacheConfig(m == 1 ? cudaFuncCachePreferShared : m == 2 ? cudaFuncCachePreferL1
+                                                                                   : cudaFuncCachePreferNone));
+        }
         {
             cudaMemPool_t pool;
             CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -907,7 +913,7 @@ scoup_status scoup_uplift_init_levels(int device, void* cuda_stream, int64_t num
         const int64_t G = std::max<int64_t>(1, num_gaussians);
         dalloc(&h->pg.a, G, hs);
         dalloc(&h->pg.b, G, hs);
-        dalloc(&h->pg.c, G, hs);
+        dalloc(&h->pg.c, G + 1, hs);  // (preprocess reads the aligned 16 B holding c[i])
         dalloc(&h->pg.s2, G, hs);
         if (const char* nf = std::getenv("SCOUP_NEAR_FRAC")) {
             const double f = std::atof(nf);

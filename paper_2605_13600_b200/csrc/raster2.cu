@@ -87,6 +87,9 @@ struct __align__(16) R2Smem {
     int overflow;
     int wcnt[2][R2W];  // accepted candidates per warp, double-buffered over refill rounds
     unsigned long long contrib, tests, evals, reds;
+#ifdef RASTER2_PAD
+    unsigned char pad[RASTER2_PAD];  // (A/B: residency limited by shared memory at a given register count)
+#endif
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -434,19 +437,26 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
             // ---- flush: S reds per (slot, record) into W, one per record into Z (sum over slots)
             const int ncol = nsub * BATCH;
             auto gid_of = [&](int j) { return __float_as_uint(sm.re[ring_wrap(q_head + (uint32_t)j)].z); };
-            const int nitems = nslot * R2SB * S;
+            // two threads per (slot, record): the pair's sum once, then the thread's half of the
+            // S atoms (s = parity, parity + 2, ...)
+            const int nitems = nslot * R2SB * 2;
             for (int i = t; i < nitems; i += R2T) {
-                const uint32_t u = s_log2 >= 0 ? (uint32_t)i >> s_log2 : __umulhi((uint32_t)i, s_magic);  // (slot, record)
-                const int j = (int)(u & (R2SB - 1)), q = (int)(u / R2SB), s = i - (int)u * S;
+                const int u = i >> 1;  // (slot, record)
+                const int j = u & (R2SB - 1), q = u / R2SB;
                 if (j >= ncol) continue;
                 float v = sm.acc[buf][u];
 #pragma unroll
                 for (int w = 0; w < R2W; w++)
                     if (ws[w] == q) v += sm.accw[buf][w][j];
-                const uint32_t a = sm.slot_atom[q][s];
-                if (v > 0.f && a != NONE) {
-                    if (COUNT) nred++;
-                    atomicAdd(p.W + (int64_t)gid_of(j) * L + a, __fmul_rn(sm.slot_coef[q][s], v));
+                if (v > 0.f) {
+                    float* const Wg = p.W + (int64_t)gid_of(j) * L;
+                    for (int s = i & 1; s < S; s += 2) {
+                        const uint32_t a = sm.slot_atom[q][s];
+                        if (a != NONE) {
+                            if (COUNT) nred++;
+                            atomicAdd(Wg + a, __fmul_rn(sm.slot_coef[q][s], v));
+                        }
+                    }
                 }
             }
             if (t < ncol) {
@@ -528,13 +538,19 @@ static int raster2_slots(const RasterParams& p) {
 
 template <int R2S>
 static void launch_raster2_slots(const RasterParams& p, int nblocks, cudaStream_t s) {
+#ifndef RASTER2_PAD
     static_assert(RASTER2_MIN_BLOCKS * (sizeof(R2Smem<R2S>) + 1024) <= 228 * 1024, "shared memory per SM");
+#endif
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(raster2_kernel<true, R2S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(R2Smem<R2S>));
         cudaFuncSetAttribute(raster2_kernel<false, R2S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(R2Smem<R2S>));
+        if (const char* e = getenv("SCOUP_RASTER2_CARVEOUT")) {  // (A/B) percent of the L1 / shared array
+            cudaFuncSetAttribute(raster2_kernel<true, R2S>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+            cudaFuncSetAttribute(raster2_kernel<false, R2S>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+        }
         attr_set = true;
     }
     if (p.count_tests) raster2_kernel<true, R2S><<<nblocks, R2T, sizeof(R2Smem<R2S>), s>>>(p);
