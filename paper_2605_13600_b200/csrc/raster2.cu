@@ -53,6 +53,10 @@ constexpr int R2Q = RASTER2_RING;
 #endif
 constexpr int R2SB = RASTER2_NSUB * BATCH;    // records per super-batch (one barrier, one flush)
 constexpr int RG = 8;                         // records per warp-uniform group (and per reduction)
+#ifndef RASTER2_FLUSH_SPLIT
+#define RASTER2_FLUSH_SPLIT 2                 // threads per (slot, record) in the flush (a power of two)
+#endif
+constexpr int R2FS = RASTER2_FLUSH_SPLIT;
 #ifndef RASTER2_MIN_BLOCKS
 #define RASTER2_MIN_BLOCKS 7
 #endif
@@ -437,11 +441,11 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
             // ---- flush: S reds per (slot, record) into W, one per record into Z (sum over slots)
             const int ncol = nsub * BATCH;
             auto gid_of = [&](int j) { return __float_as_uint(sm.re[ring_wrap(q_head + (uint32_t)j)].z); };
-            // two threads per (slot, record): the pair's sum once, then the thread's half of the
-            // S atoms (s = parity, parity + 2, ...)
-            const int nitems = nslot * R2SB * 2;
+            // R2FS threads per (slot, record): the pair's sum once per thread, then the thread's
+            // share of the S atoms (s = i mod R2FS, + R2FS, ...)
+            const int nitems = nslot * R2SB * R2FS;
             for (int i = t; i < nitems; i += R2T) {
-                const int u = i >> 1;  // (slot, record)
+                const int u = i / R2FS;  // (slot, record)
                 const int j = u & (R2SB - 1), q = u / R2SB;
                 if (j >= ncol) continue;
                 float v = sm.acc[buf][u];
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(R2T, RASTER2_MIN_BLOCKS) raster2_kernel(const 
                     if (ws[w] == q) v += sm.accw[buf][w][j];
                 if (v > 0.f) {
                     float* const Wg = p.W + (int64_t)gid_of(j) * L;
-                    for (int s = i & 1; s < S; s += 2) {
+                    for (int s = i & (R2FS - 1); s < S; s += R2FS) {
                         const uint32_t a = sm.slot_atom[q][s];
                         if (a != NONE) {
                             if (COUNT) nred++;

@@ -30,10 +30,29 @@ MARKERS = [  # (region, regex of the first line)
 ]
 
 
-def regions_of_raster():
-    lines = open(os.path.join(ROOT, "paper_2605_13600_b200", "csrc", "raster.cu")).read().splitlines()
+MARKERS2 = [  # raster2.cu (the production kernel)
+    ("transpose8", r"^__device__ __forceinline__ float transpose8"),
+    ("pass_select", r"^__device__ __forceinline__ float pass_select"),
+    ("overflow", r"^__device__ __noinline__ void overflow_red1"),
+    ("setup", r"^__global__ void __launch_bounds__\(R2T"),
+    ("refill", r"// ---- refill the ring"),
+    ("superbatch_head", r"const uint32_t n = min\(\(uint32_t\)R2SB, q_count\);"),
+    ("warp_band_test", r"const uint32_t sh = "),
+    ("group_loop_head", r"for \(int g0 = 0; g0 < BATCH; g0 \+= RG\)"),
+    ("pixel_loop", r"float eA\[RG\], eB\[RG\];"),
+    ("reduce+smem_acc", r"// ---- reduce the group's weights"),
+    ("barrier", r"// the super-batch's sums are complete"),
+    ("flush", r"// ---- flush: S reds per"),
+    ("flush_zero+advance", r"// zero the buffer of super-batch i\+2"),
+    ("epilogue", r"cp_async_wait_all\(\);  // no copy may land"),
+]
+
+
+def regions_of_raster(fname="raster.cu", markers=None, text=None):
+    markers = markers or MARKERS
+    lines = (text or open(os.path.join(ROOT, "paper_2605_13600_b200", "csrc", fname)).read()).splitlines()
     starts = []
-    for name, rx in MARKERS:
+    for name, rx in markers:
         for i, ln in enumerate(lines, 1):
             if re.search(rx, ln):
                 starts.append((i, name))
@@ -51,6 +70,12 @@ def region(file, line, starts):
             if m:
                 return "internal:" + m.group(1)
         return "internal"
+    if file == "raster2.cu" and STARTS2:
+        name = "other"
+        for s, n in STARTS2:
+            if line >= s:
+                name = n
+        return "r2:" + name
     if file != "raster.cu":
         return file
     name = "other"
@@ -60,7 +85,17 @@ def region(file, line, starts):
     return name
 
 
-def main(path):
+STARTS2 = []
+
+
+def main(path, rev=None):
+    global STARTS2
+    # raster2.cu as profiled: the working tree, or `rev` (a git revision) when the capture is older
+    text = None
+    if rev:
+        text = subprocess.run(["git", "-C", ROOT, "show", f"{rev}:paper_2605_13600_b200/csrc/raster2.cu"],
+                              capture_output=True, text=True).stdout
+    STARTS2 = regions_of_raster("raster2.cu", MARKERS2, text)
     out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     starts = regions_of_raster()
@@ -90,4 +125,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
