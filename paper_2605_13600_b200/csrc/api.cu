@@ -107,6 +107,7 @@ struct Ctx {
     cudaStream_t rs = nullptr;    // its raster launches (low priority), joined back into s
     cudaEvent_t ev = nullptr;     // end of the last enqueued step (the host waits on it)
     cudaEvent_t ev_rs0 = nullptr, ev_rs1 = nullptr;  // s -> rs -> s hand-offs around a raster
+    int map_ch0 = 0, map_ch1 = -1;  // host-map copy chunks the batch's rasters wait for (none: ch1 < ch0)
     ViewBuffers vb{};
     size_t g_cap = 0, s_cap = 0, e_cap = 0, t_cap = 0, px_cap = 0, tl_cap = 0, bc_cap = 0, eb_cap = 0, ee_cap = 0;
     void* cub_tmp = nullptr;
@@ -627,6 +628,8 @@ scoup_status chunk_back(scoup_uplift* h, Ctx& c, const CallArgs& a, int chunk, i
     // the raster on the context's low-priority stream, joined back before the next step
     CK(cudaEventRecord(c.ev_rs0, c.s));
     CK(cudaStreamWaitEvent(c.rs, c.ev_rs0, 0));
+    // only the raster reads the region maps: the batch's front runs while its chunk is still in flight
+    for (int j = c.map_ch0; j <= c.map_ch1; j++) CK(cudaStreamWaitEvent(c.rs, h->chunk_ev[j], 0));
     ev_mark(c, mark0, c.rs);
     if (a.render) launch_render(p, c.rs);
     else if (h->raster_kernel != 1 && raster2_supported(p)) launch_raster2(p, c.rs);
@@ -761,8 +764,11 @@ scoup_status run_views(scoup_uplift* h, int32_t num_views, const scoup_camera* c
             }
             if (!ids_on_device && nlev > 0) {  // this batch's chunks of the host-map copy
                 copy_ahead((c.v0 + c.nv - 1) / MAX_VB + 3);
-                for (int j = c.v0 / MAX_VB; j <= (c.v0 + c.nv - 1) / MAX_VB; j++)
-                    CK(cudaStreamWaitEvent(c.s, h->chunk_ev[j], 0));
+                c.map_ch0 = c.v0 / MAX_VB;
+                c.map_ch1 = (c.v0 + c.nv - 1) / MAX_VB;
+            } else {
+                c.map_ch0 = 0;
+                c.map_ch1 = -1;
             }
             for (int v = 0; v < c.nv; v++) {
                 const int u = c.v0 + v;
